@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark: SRHT sketch throughput of [A | b] (input GB/s and fraction of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl srht|reference]
+
+Default workload: BASELINE.json config 5 (A = 2^26 x 127 FP32 Uniform[0,1) plus b,
+128 columns, 34.4 GB, r = 16384), the configuration the metric is quoted on at
+1/2/4/8 GPUs.  One "step" = one SRHT sketch of all 128 columns: the tile kernel
+(load + sign + FWHT + pruned accumulate) and the slab reduction, plus, for N > 1,
+one NCCL all_gather of the r x c_g shards (columns are sharded across ranks;
+total work is fixed, so scaling is "strong").  Plan creation (Algorithm 1 steps
+2 and 4) is excluded, as in SURVEY.md 8(d).  Inputs (34 GB) are far larger than
+L2 (126 MB), so no L2 flush is needed between steps.
+
+Under torchrun every rank runs its shard; timing is CUDA events on the launch
+stream between barriers + synchronize, max over ranks; rank 0 prints one JSON line.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "SRHT sketch throughput: input GB/s of [A|b] and % of B200 HBM peak, 1/2/4/8 GPUs"
+UNIT = "GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="srht", choices=["srht", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def column_range(c, world, rank):
+    base, rem = divmod(c, world)
+    c0 = rank * base + min(rank, rem)
+    return c0, c0 + base + (1 if rank < rem else 0)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured", d
+    except Exception:
+        return 6650.0, "fallback", {}
+
+
+def load_traffic(config):
+    """dram read+write bytes per launch of the tile kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("config%d" % config)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                "gpu_idle": getattr(pynvml, "nvmlClocksEventReasonGpuIdle", 0x1),
+                "applications_clocks_setting": getattr(pynvml, "nvmlClocksEventReasonApplicationsClocksSetting", 0x2),
+                "sw_power_cap": getattr(pynvml, "nvmlClocksEventReasonSwPowerCap", 0x4),
+                "hw_slowdown": getattr(pynvml, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                "sync_boost": 0x10,
+                "sw_thermal_slowdown": 0x20,
+                "hw_thermal_slowdown": 0x40,
+                "hw_power_brake_slowdown": 0x80,
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for k, v in names.items():
+                            if mask & v and k != "gpu_idle":
+                                self.reasons.add(k)
+                    except Exception:
+                        pass
+                    time.sleep(0.02)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+            self.ok = True
+        except Exception:
+            self.ok = False
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "note": "NVML sampling unavailable"}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# Oracle timing (cpu_baseline leg and --impl reference): the only places bench
+# executes oracle/.
+# ---------------------------------------------------------------------------
+
+def oracle_sample(cfg_id, seed=workloads.SEED):
+    """One bounded sample of the workload for the CPU oracle: (callable, bytes, description)."""
+    from oracle import srht as osr
+    cfg = workloads.CONFIGS[cfg_id]
+    n, r = cfg["n"], cfg["r"]
+    if cfg["kind"] == "dense":
+        col = workloads.host_uniform_column(seed, 0, n).astype(np.float64)
+        return (lambda: osr.sketch(col, seed, r)), 4 * n, "1 column (A[:,0]) of config %d, n=%d, r=%d" % (cfg_id, n, r)
+    if cfg_id == 3:
+        w = workloads.config3_host(seed)
+        dense = workloads.csc_to_dense(w["colptr"], w["rowidx"], w["vals"], n, 4)
+        nbytes = 8 * int(w["colptr"][4]) + 8 * 5
+        return (lambda: osr.sketch(dense, seed, r)), nbytes, "4 CSC columns of config 3 (densified), n=%d, r=%d" % (n, r)
+    w = workloads.config2_host(seed, batch=2)
+    c = w["d"] + 1
+    dense = workloads.csc_to_dense(w["colptr"], w["rowidx"], w["vals"], n, 2 * c)
+    nbytes = 8 * int(w["colptr"][2 * c]) + 8 * (2 * c + 1)
+
+    def run():
+        for p in range(2):
+            osr.sketch(dense[:, p * c:(p + 1) * c], seed, r, p=p)
+    return run, nbytes, "2 of 3000 batched CSC problems of config 2 (densified), n=%d, r=%d" % (n, r)
+
+
+def time_oracle(cfg_id, reps=1):
+    fn, nbytes, desc = oracle_sample(cfg_id)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    t = min(ts)
+    return nbytes / t / 1e9, t, desc
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = workloads.CONFIGS[args.config]
+    fn, nbytes, desc = oracle_sample(args.config)
+    for _ in range(args.warmup):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fn()
+    t = (time.perf_counter() - t0) / args.steps
+    value = nbytes / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config%d_%s" % (args.config, cfg["name"]), "n": cfg["n"], "d": cfg["d"],
+                   "r": cfg["r"], "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# The GPU arm
+# ---------------------------------------------------------------------------
+
+def build_dense_shard(cfg, c0, c1, seed, device, srht):
+    """Column shard [c0, c1) of M = [A | b] on the device (A generated, b = A x + noise)."""
+    import torch
+    n, d = cfg["n"], cfg["d"]
+    c = d + 1
+    Ml = torch.empty((c1 - c0, n), dtype=torch.float32, device=device).t()
+    a1 = min(c1, d)
+    if a1 > c0:
+        srht.gen_uniform(seed, c0, Ml[:, : a1 - c0])
+    if c1 == c:  # this rank holds b
+        x = workloads.x_true_half_zeros(seed, d)
+        e = workloads._rng(seed, 2).standard_normal(n) * 0.01
+        b64 = torch.from_numpy(e).to(device)
+        xt = torch.from_numpy(x).to(device)
+        chunk = 8
+        tmp = torch.empty((chunk, n), dtype=torch.float32, device=device).t()
+        for j0 in range(0, d, chunk):
+            j1 = min(d, j0 + chunk)
+            if c0 <= j0 and j1 <= a1:
+                blk = Ml[:, j0 - c0:j1 - c0]
+            else:
+                blk = tmp[:, : j1 - j0]
+                srht.gen_uniform(seed, j0, blk)
+            b64 += blk.double() @ xt[j0:j1]
+        Ml[:, c - 1 - c0] = b64.float()
+        del tmp, b64
+    torch.cuda.synchronize()
+    return Ml
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_0812_4547_b200 as srht
+    from paper_0812_4547_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    cfg = workloads.CONFIGS[args.config]
+    if cfg["kind"] != "dense":
+        raise SystemExit("bench.py measures the dense configs (1, 4, 5); sparse configs are covered by tests")
+    n, d, r, seed = cfg["n"], cfg["d"], cfg["r"], workloads.SEED
+    c = d + 1
+    c0, c1 = column_range(c, world, rank)
+    cl = c1 - c0
+    Ml = build_dense_shard(cfg, c0, c1, seed, device, srht)
+    plan = srht.Plan(n, d, r, seed)
+    ws = plan.workspace(cl)
+    cmax = (c + world - 1) // world
+    local_out = torch.zeros((cmax, r), dtype=torch.float32, device=device)  # row-major [col][t] = col-major r x c
+    gathered = torch.empty((world * cmax, r), dtype=torch.float32, device=device) if world > 1 else None
+    stream = torch.cuda.current_stream(device)
+    lib = _lib.load()
+
+    def step():
+        plan.sketch_columns(Ml, out=local_out[:cl].t(), workspace=ws)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, local_out)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+
+    # per-step events around the tile kernel (library profiling hook)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            lib.srht_profile_set_events(kev[i][0].cuda_event, kev[i][1].cuda_event)
+            step()
+        ev1.record(stream)
+        lib.srht_profile_set_events(None, None)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    kms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    t = torch.tensor([ms, kms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, kms_max = float(t[0]), float(t[1])
+
+    total_in = 4.0 * n * c
+    value = total_in / (ms * 1e-3) / 1e9
+    peak, peak_kind, peaks = load_peaks()
+    alg_bytes_launch = 4.0 * n * cl + 4.0 * r * cl  # read the shard once, write r x c_l
+    achieved = alg_bytes_launch / (kms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": load_traffic(args.config), "kernel": "k_sketch_tiles",
+                "peak_source": "%s (MEASURED_PEAKS.json hbm_gbs)" % peak_kind if peak_kind == "measured"
+                else "fallback 6650 GB/s (B200_PROFILING.md)",
+                "kernel_ms": kms, "share_of_step": kms / ms}
+
+    # ---- e2e: the same sketch through the host-buffer C-ABI call ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device)
+
+    # ---- cpu_baseline: the oracle on the host cores (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, tsec, desc = time_oracle(args.config)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc, "seconds": tsec}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config%d_%s" % (args.config, cfg["name"]), "n": n, "d": d, "r": r,
+                       "columns": c, "input_bytes": total_in, "parallelism": "columns/%d" % world,
+                       "l2": "inputs larger than L2 (no flush)" if total_in > 2 * 126e6 else "flushed"},
+            "hbm_frac_of_measured": value / peak,
+            "hbm_frac_of_8TBs": value / 8000.0,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps * (2 if plan_has_reduce(plan) else 1),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def plan_has_reduce(plan):
+    return plan.workspace_bytes(1) > 0
+
+
+def measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device):
+    """Host-buffer end-to-end: pinned host [A|b] shard -> device -> sketch -> host, every step."""
+    import psutil
+    import torch
+    import torch.distributed as dist
+    need = 4 * n * cl
+    avail = psutil.virtual_memory().available
+    cols = cl
+    if need > 0.6 * avail:
+        cols = max(1, int(0.6 * avail // (4 * n)))
+    host = torch.empty((cols, n), dtype=torch.float32).pin_memory().t()
+    host.copy_(Ml[:, :cols])
+    out = torch.empty((cols, r), dtype=torch.float32).pin_memory().t()
+    plan.sketch_columns_host(host, out=out)  # warm-up
+    if world > 1:
+        dist.barrier()
+    ts = []
+    for _ in range(max(1, args.e2e_steps)):
+        t0 = time.perf_counter()
+        plan.sketch_columns_host(host, out=out)
+        ts.append(time.perf_counter() - t0)
+    t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t[0])
+    total_cols = cols * world
+    e2e = {"value": 4.0 * n * total_cols / sec / 1e9, "unit": UNIT, "h2d_bytes_per_step": 4 * n * cols,
+           "d2h_bytes_per_step": 4 * r * cols, "seconds_per_step": sec,
+           "api": "srht_sketch_columns_host (pinned host buffers, chunked H2D/sketch/D2H pipeline)"}
+    if cols < cl:
+        e2e["sample"] = "%d of %d columns per rank (host RAM %.0f GB available)" % (cols, cl, avail / 1e9)
+    del host
+    return e2e
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/*
+ * srht.h -- C ABI of the B200 SRHT sketch (hot path of RandomizedNNLS,
+ * arXiv 0812.4547, "Random projections for the nonnegative least-squares
+ * problem").
+ *
+ * What it computes (Algorithm 1, and the proof's
+ * Phi = [H_n D A, -H_n D b]):
+ *
+ *     SM[t, j] = sqrt(N/r) * (H_N/sqrt(N) * D * [M ; 0])[k_t, j]
+ *              = r^{-1/2} * sum_{i<n} (-1)^{popc(k_t & i)} * sigma_i * M[i, j]
+ *
+ * for every column j of M = [A | b] (n x (d+1)), with
+ *   N        = smallest power of two >= max(n, 2) (zero padding),
+ *   sigma_i  = +-1 diagonal of D (Algorithm 1 step 4),
+ *   k_0<...<k_{r-1} = the kept rows of S H_N (steps 2-3),
+ *   H_N[k,i] = (-1)^{popc(k & i)} (Sylvester recursion of P:154-165).
+ * The same D and the same kept rows act on every column.
+ *
+ * Readings where the paper is silent (R1-R14): exactly r distinct
+ * rows (R1); the padded N is the n of sqrt(n/r) (R2); Philox4x64-10 streams
+ * (R4): word w of stream (seed, 2p + tag) is word (w mod 4) of
+ * philox4x64_10(ctr = (1 + w/4, 0, 0, 0), key = (seed, 2p + tag)); sigma_i = -1
+ * iff bit (i mod 64) of word i/64 of tag 0 is set (R5); k = the r indices with
+ * the smallest (word i of tag 1, i), sorted ascending (R6).  p is the problem
+ * index (0 for a single problem).
+ *
+ * Conventions for every entry point:
+ *   - Matrix/vector pointers passed to srht_sketch* are DEVICE pointers owned by
+ *     the caller; inputs are read-only, outputs write-only.  The plan owns only
+ *     its own device buffers (sign words, kept rows).
+ *   - srht_sketch* enqueue work on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream) and return without synchronizing.
+ *     Asynchronous faults surface at the caller's next synchronization.
+ *   - srht_plan_create* are synchronous on the current CUDA device.
+ *   - Scratch memory is caller-provided (srht_workspace_bytes); srht_sketch*
+ *     never allocate, so concurrent calls on different streams with different
+ *     workspaces are safe.  A plan is immutable after creation.
+ *   - Invalid arguments return SRHT_EINVAL before any launch; launch failures
+ *     return SRHT_ECUDA.  Non-finite input values are not checked.
+ *   - Arithmetic: FP32 inputs, FP32 adds (round to nearest), FP32 outputs;
+ *     the final r^{-1/2} is applied once, in FP32, to the FP32 sum.
+ */
+#ifndef SRHT_H_
+#define SRHT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct srht_plan srht_plan; /* opaque, immutable after create */
+
+typedef enum {
+  SRHT_OK = 0,
+  SRHT_EINVAL = 1,       /* bad argument (checked before any launch)        */
+  SRHT_ENOMEM = 2,       /* device allocation failed (plan creation only)   */
+  SRHT_ECUDA = 3,        /* a CUDA call or kernel launch failed             */
+  SRHT_EUNSUPPORTED = 4  /* valid but outside this build's limits           */
+} srht_status;
+
+enum { SRHT_DENSE = 0, SRHT_CSC = 1 };
+
+/* A device matrix with `rows` rows and `cols` columns.
+ * SRHT_DENSE: column-major FP32, element (i, j) at vals[i + j*ld], ld >= rows.
+ * SRHT_CSC:   column j holds entries colptr[j] .. colptr[j+1]-1 of
+ *             (rowidx, vals); colptr has cols+1 int64 entries (colptr[0] may be
+ *             non-zero); rowidx is int32, sorted ascending within a column,
+ *             0 <= rowidx < rows; duplicate row indices are summed.          */
+typedef struct {
+  int32_t fmt;
+  int64_t rows, cols;
+  const float* vals;
+  int64_t ld;
+  const int64_t* colptr;
+  const int32_t* rowidx;
+  int64_t nnz;
+} srht_matrix;
+
+/* Build the plan of one problem (p = 0): n rows, d columns of A (the sketch
+ * accepts any column count; d is recorded for srht_sketch), r kept rows,
+ * Philox seed.  Requires n >= 1, d >= 0, 1 <= r <= N, N <= 2^30.
+ * Algorithm 1 steps 2 and 4, computed on the device.            */
+srht_status srht_plan_create(int64_t n, int64_t d, int64_t r, uint64_t seed,
+                             srht_plan** out);
+
+/* `batch` independent problems of the same shape; problem p uses streams
+ * (seed, 2p) and (seed, 2p+1), i.e. its own D and kept rows.                 */
+srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r,
+                                     uint64_t seed, int64_t batch,
+                                     srht_plan** out);
+
+srht_status srht_plan_destroy(srht_plan* plan); /* NULL is a no-op */
+
+/* N (padded size), r and batch of a plan; any output pointer may be NULL.    */
+srht_status srht_plan_info(const srht_plan* plan, int64_t* N, int64_t* r,
+                           int64_t* batch);
+
+/* Kept rows of problem p, ascending, into host memory (r int32 values).     */
+srht_status srht_plan_copy_indices(const srht_plan* plan, int64_t problem,
+                                   int32_t* host_K);
+
+/* Sign words of problem p into host memory: ceil(N/64) uint64 words, bit
+ * (i mod 64) of word i/64 set iff sigma_i = -1.                              */
+srht_status srht_plan_copy_signs(const srht_plan* plan, int64_t problem,
+                                 uint64_t* host_words);
+
+/* Device scratch bytes needed by srht_sketch* for `ncols` columns (the
+ * per-slab partial sums of the multi-pass path; 0 when not needed).  The
+ * workspace must be 256-byte aligned.                                        */
+size_t srht_workspace_bytes(const srht_plan* plan, int64_t ncols);
+
+/* Sketch one problem: SA (r x A->cols, column-major, ldsa >= r) = H~ D A and
+ * Sb (r) = H~ D b (Algorithm 1 step 5 inputs).  A->rows and b->rows
+ * must equal the plan's n; b must have exactly one column.  b may be NULL
+ * (then Sb is ignored).  A and b may be dense or CSC independently.          */
+srht_status srht_sketch(const srht_plan* plan, const srht_matrix* A,
+                        const srht_matrix* b, float* SA, int64_t ldsa,
+                        float* Sb, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+/* Sketch every column of M (rows == n, any column count) into SM (r x cols,
+ * ldsm >= r).  Columns are independent, so a column range of [A | b] is the
+ * multi-GPU shard primitive; results do not depend on the range (the tile and
+ * slab geometry depend only on n and r).                                     */
+srht_status srht_sketch_columns(const srht_plan* plan, const srht_matrix* M,
+                                float* SM, int64_t ldsm, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/* Batched mode: M has batch*c columns (problem p owns columns p*c .. p*c+c-1,
+ * c = M->cols / batch); output SM is batch blocks of r x c, column-major and
+ * contiguous (column g of M lands at SM + g*r).  Problem p uses its own plan.  */
+srht_status srht_sketch_batched(const srht_plan* plan, const srht_matrix* M,
+                                float* SM, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/* Same as srht_sketch_columns, but M's values, column pointers, row indices
+ * and SM are HOST buffers (pinned or pageable).  Host->device copies, the
+ * sketch and the device->host copy run inside the call, pipelined over column
+ * chunks on internal streams; returns after SM is written (synchronous).
+ * Device memory is allocated internally per call.                            */
+srht_status srht_sketch_columns_host(const srht_plan* plan,
+                                     const srht_matrix* M_host, float* SM_host,
+                                     int64_t ldsm);
+
+const char* srht_status_str(srht_status s);
+
+/* ---- Profiling hook (benchmark instrumentation) ----
+ * When set, every subsequent srht_sketch* call records `before` and `after`
+ * (cudaEvent_t passed as void*) on its stream immediately around the main
+ * tile kernel (k_sketch_tiles), so its duration can be timed with CUDA events
+ * on the stream it runs on.  Pass NULL, NULL to clear.  Process-global, not
+ * thread-safe; events must belong to the plan's device.                       */
+srht_status srht_profile_set_events(void* before, void* after);
+
+/* ---- Workload generator (benchmark / test input only; not the method) ----
+ * out[i + j*ld] = (word i of stream (seed, 2^32 + stream0 + j) >> 40) * 2^-24,
+ * i.e. exact FP32 Uniform[0,1) values from the same Philox stream convention,
+ * for i < rows, j < cols (device pointer, async on stream).                 */
+srht_status srht_gen_uniform(uint64_t seed, uint64_t stream0, int64_t rows,
+                             int64_t cols, float* out, int64_t ld,
+                             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRHT_H_ */

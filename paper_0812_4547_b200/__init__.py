@@ -1,0 +1,254 @@
+"""B200-native SRHT sketch of [A | b] -- the hot path of RandomizedNNLS (arXiv 0812.4547).
+
+Thin Python binding over the C ABI in ``include/srht.h`` (``libsrht.so``, built
+in-tree for sm_100a).  Every step of the sketch runs in the library's CUDA
+kernels; this module only marshals torch tensors into pointers, sizes and the
+current CUDA stream.  There is no CPU fallback: importing works without a GPU
+(so the ABI can be inspected), but every call needs a CUDA device.
+
+    plan = Plan(n, d, r, seed)            # Algorithm 1 steps 2 and 4 (device)
+    SA, Sb = plan.sketch(A, b)            # H~ D A and H~ D b (step 5 inputs)
+
+Dense inputs are column-major FP32 CUDA tensors of shape (n, c) (stride(0) == 1);
+sparse inputs are ``CSC`` triples or ``torch.sparse_csc`` tensors.  Outputs are
+column-major (r, c) FP32 tensors.
+"""
+
+import ctypes
+from collections import namedtuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import SRHT_CSC, SRHT_DENSE, SrhtMatrix, SrhtError, check
+
+__all__ = ["Plan", "CSC", "SrhtError", "colmajor", "gen_uniform", "padded_size", "library"]
+
+CSC = namedtuple("CSC", ["colptr", "rowidx", "vals", "shape"])
+CSC.__doc__ = "Compressed sparse columns: int64 colptr[c+1], int32 rowidx[nnz] (sorted per column), float32 vals."
+
+
+def library():
+    """The loaded ctypes library (raises ImportError if it was not built)."""
+    return _lib.load()
+
+
+def padded_size(n):
+    N = 2
+    while N < n:
+        N *= 2
+    return N
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def colmajor(x):
+    """Column-major copy/view of a 2-D tensor (no copy if already column-major)."""
+    if x.dim() == 1:
+        return x.reshape(-1, 1)
+    if x.stride(0) == 1 and (x.shape[1] <= 1 or x.stride(1) >= x.shape[0]):
+        return x
+    return x.t().contiguous().t()
+
+
+def _stream_ptr(device):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _as_csc(M):
+    torch = _torch()
+    if isinstance(M, CSC):
+        return M
+    if isinstance(M, torch.Tensor) and M.layout == torch.sparse_csc:
+        return CSC(M.ccol_indices().to(torch.int64), M.row_indices().to(torch.int32),
+                   M.values().to(torch.float32), tuple(M.shape))
+    return None
+
+
+def _describe(M, keep):
+    """srht_matrix for a device tensor / CSC; `keep` collects tensors to keep alive."""
+    torch = _torch()
+    csc = _as_csc(M)
+    if csc is not None:
+        colptr = csc.colptr.to(torch.int64).contiguous()
+        rowidx = csc.rowidx.to(torch.int32).contiguous()
+        vals = csc.vals.to(torch.float32).contiguous()
+        keep += [colptr, rowidx, vals]
+        rows, cols = int(csc.shape[0]), int(csc.shape[1])
+        for t in (colptr, rowidx, vals):
+            if not t.is_cuda:
+                raise ValueError("CSC arrays must be CUDA tensors")
+        return SrhtMatrix(SRHT_CSC, rows, cols, vals.data_ptr(), max(rows, 1), colptr.data_ptr(),
+                          rowidx.data_ptr(), int(vals.numel()))
+    if not isinstance(M, torch.Tensor) or not M.is_cuda:
+        raise ValueError("dense input must be a CUDA tensor")
+    if M.dtype != torch.float32:
+        raise ValueError("dense input must be float32")
+    M = colmajor(M)
+    keep.append(M)
+    rows, cols = int(M.shape[0]), int(M.shape[1])
+    ld = int(M.stride(1)) if cols > 1 else max(rows, 1)
+    return SrhtMatrix(SRHT_DENSE, rows, cols, M.data_ptr(), max(ld, rows, 1), None, None, 0)
+
+
+class Plan:
+    """Plan of Algorithm 1's random matrices D and S for `batch` problems of shape n x d.
+
+    Created on the current CUDA device (synchronous).  `seed` selects the
+    Philox streams (R4); problem p uses streams (seed, 2p), (seed, 2p+1).
+    """
+
+    def __init__(self, n, d, r, seed=0, batch=1):
+        self._lib = _lib.load()
+        self._h = ctypes.c_void_p()
+        check(self._lib.srht_plan_create_batched(int(n), int(d), int(r), ctypes.c_uint64(int(seed) & (2**64 - 1)),
+                                                 int(batch), ctypes.byref(self._h)), "srht_plan_create_batched")
+        N, rr, bb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(self._lib.srht_plan_info(self._h, ctypes.byref(N), ctypes.byref(rr), ctypes.byref(bb)), "srht_plan_info")
+        self.n, self.d, self.r, self.N, self.batch, self.seed = int(n), int(d), int(rr.value), int(N.value), int(bb.value), int(seed)
+        torch = _torch()
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self._ws = None
+
+    # -- lifetime --
+    def close(self):
+        if self._h:
+            self._lib.srht_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- introspection --
+    def indices(self, problem=0):
+        out = np.empty(self.r, dtype=np.int32)
+        check(self._lib.srht_plan_copy_indices(self._h, int(problem), out.ctypes.data), "srht_plan_copy_indices")
+        return out
+
+    def sign_words(self, problem=0):
+        out = np.empty((self.N + 63) // 64, dtype=np.uint64)
+        check(self._lib.srht_plan_copy_signs(self._h, int(problem), out.ctypes.data), "srht_plan_copy_signs")
+        return out
+
+    def workspace_bytes(self, ncols):
+        return int(self._lib.srht_workspace_bytes(self._h, int(ncols)))
+
+    def workspace(self, ncols):
+        nb = self.workspace_bytes(ncols)
+        if nb == 0:
+            return None
+        torch = _torch()
+        if self._ws is None or self._ws.numel() < nb:
+            self._ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _ws_args(self, ncols, workspace):
+        nb = self.workspace_bytes(ncols)
+        if nb == 0:
+            return None, 0
+        ws = workspace if workspace is not None else self.workspace(ncols)
+        return ws.data_ptr(), int(ws.numel())
+
+    def _out(self, rows, cols, out):
+        torch = _torch()
+        if out is None:
+            return torch.empty((cols, rows), dtype=torch.float32, device=self.device).t()
+        if out.dtype != torch.float32 or not out.is_cuda or out.stride(0) != 1:
+            raise ValueError("output must be a column-major float32 CUDA tensor")
+        return out
+
+    # -- the sketch --
+    def sketch(self, A, b=None, SA=None, Sb=None, workspace=None):
+        """(H~ D A, H~ D b) with one shared plan (Algorithm 1 step 5)."""
+        keep = []
+        dA = _describe(A, keep)
+        SA = self._out(self.r, dA.cols, SA)
+        db, sb_ptr = None, None
+        if b is not None:
+            if _as_csc(b) is None and b.dim() == 1:
+                b = b.reshape(-1, 1)
+            db = _describe(b, keep)
+            torch = _torch()
+            if Sb is None:
+                Sb = torch.empty(self.r, dtype=torch.float32, device=self.device)
+            sb_ptr = Sb.data_ptr()
+        ncols = dA.cols + (1 if b is not None else 0)
+        ws, wsb = self._ws_args(ncols, workspace)
+        ldsa = int(SA.stride(1)) if SA.shape[1] > 1 else self.r
+        check(self._lib.srht_sketch(self._h, ctypes.byref(dA), ctypes.byref(db) if db is not None else None,
+                                    SA.data_ptr(), ldsa, sb_ptr, ws, wsb, _stream_ptr(self.device)), "srht_sketch")
+        return SA, Sb
+
+    def sketch_columns(self, M, out=None, workspace=None):
+        """H~ D M for every column of M (the column-shard primitive)."""
+        keep = []
+        dM = _describe(M, keep)
+        SM = self._out(self.r, dM.cols, out)
+        ws, wsb = self._ws_args(dM.cols, workspace)
+        ld = int(SM.stride(1)) if SM.shape[1] > 1 else self.r
+        check(self._lib.srht_sketch_columns(self._h, ctypes.byref(dM), SM.data_ptr(), ld, ws, wsb,
+                                            _stream_ptr(self.device)), "srht_sketch_columns")
+        return SM
+
+    def sketch_batched(self, M, out=None, workspace=None):
+        """Batched problems: M has batch*c columns; returns (batch, c, r) (row t fastest)."""
+        torch = _torch()
+        keep = []
+        dM = _describe(M, keep)
+        c = dM.cols // self.batch
+        if out is None:
+            out = torch.empty((self.batch, c, self.r), dtype=torch.float32, device=self.device)
+        ws, wsb = self._ws_args(dM.cols, workspace)
+        check(self._lib.srht_sketch_batched(self._h, ctypes.byref(dM), out.data_ptr(), ws, wsb,
+                                            _stream_ptr(self.device)), "srht_sketch_batched")
+        return out
+
+    def sketch_columns_host(self, M, out=None):
+        """End-to-end call on HOST buffers (copies, sketch and read-back inside).
+
+        M: column-major float32 CPU tensor (n, c) (pinned for full PCIe speed) or a
+        CSC of CPU tensors.  Returns a column-major float32 CPU tensor (r, c).
+        """
+        torch = _torch()
+        csc = _as_csc(M)
+        if csc is not None:
+            colptr = csc.colptr.to(torch.int64).contiguous()
+            rowidx = csc.rowidx.to(torch.int32).contiguous()
+            vals = csc.vals.to(torch.float32).contiguous()
+            desc = SrhtMatrix(SRHT_CSC, int(csc.shape[0]), int(csc.shape[1]), vals.data_ptr(), max(int(csc.shape[0]), 1),
+                              colptr.data_ptr(), rowidx.data_ptr(), int(vals.numel()))
+            cols = int(csc.shape[1])
+        else:
+            M = colmajor(M)
+            if M.is_cuda or M.dtype != torch.float32:
+                raise ValueError("host input must be a float32 CPU tensor")
+            cols = int(M.shape[1])
+            ld = int(M.stride(1)) if cols > 1 else max(int(M.shape[0]), 1)
+            desc = SrhtMatrix(SRHT_DENSE, int(M.shape[0]), cols, M.data_ptr(), ld, None, None, 0)
+        if out is None:
+            out = torch.empty((cols, self.r), dtype=torch.float32).t()
+        ld_out = int(out.stride(1)) if cols > 1 else self.r
+        check(self._lib.srht_sketch_columns_host(self._h, ctypes.byref(desc), out.data_ptr(), ld_out),
+              "srht_sketch_columns_host")
+        return out
+
+
+def gen_uniform(seed, stream0, out):
+    """Fill a column-major float32 CUDA tensor with the workload generator's exact
+    Uniform[0,1) values (column j <- Philox stream (seed, 2^32 + stream0 + j))."""
+    lib = _lib.load()
+    out2 = out.reshape(-1, 1) if out.dim() == 1 else out
+    if out2.stride(0) != 1:
+        raise ValueError("gen_uniform needs a column-major tensor")
+    rows, cols = int(out2.shape[0]), int(out2.shape[1])
+    ld = int(out2.stride(1)) if cols > 1 else max(rows, 1)
+    check(lib.srht_gen_uniform(ctypes.c_uint64(seed), ctypes.c_uint64(stream0), rows, cols, out2.data_ptr(), ld,
+                               _stream_ptr(out.device)), "srht_gen_uniform")
+    return out

@@ -1,0 +1,381 @@
+// C ABI (include/srht.h): validation, plan geometry, dispatch.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace {
+
+int ceil_log2(int64_t x) {
+  int l = 0;
+  while ((int64_t(1) << l) < x) ++l;
+  return l;
+}
+
+bool valid_matrix(const srht_matrix* M) {
+  if (!M) return false;
+  if (M->rows < 0 || M->cols < 0) return false;
+  if (M->fmt == SRHT_DENSE) {
+    if (M->cols > 0 && M->rows > 0 && !M->vals) return false;
+    if (M->ld < M->rows || M->ld < 1) return false;
+    return true;
+  }
+  if (M->fmt == SRHT_CSC) {
+    if (!M->colptr) return false;
+    if (M->nnz < 0 || M->nnz > 0x7fffffffLL) return false;
+    if (M->nnz > 0 && (!M->rowidx || !M->vals)) return false;
+    if (M->rows > 0x7fffffffLL) return false;
+    return true;
+  }
+  return false;
+}
+
+srht::ColSrc make_src(const srht_matrix* M, float* out, int64_t ldo) {
+  srht::ColSrc c;
+  std::memset(&c, 0, sizeof(c));
+  c.fmt = M->fmt;
+  c.vals = M->vals;
+  c.ld = M->ld;
+  c.colptr = M->colptr;
+  c.rowidx = M->rowidx;
+  c.ncols = M->cols;
+  c.out = out;
+  c.ldo = ldo;
+  c.vec = (M->fmt == SRHT_DENSE) && (M->ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(M->vals) & 15) == 0);
+  return c;
+}
+
+size_t partial_bytes(const srht_plan* P, int64_t ncols) {
+  if (P->S_act <= 1 || ncols <= 0) return 0;
+  const size_t b = (size_t)P->S_act * (size_t)ncols * (size_t)P->r * sizeof(float);
+  return (b + 255) & ~size_t(255);
+}
+
+srht::SketchParams base_params(const srht_plan* P) {
+  srht::SketchParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.signs = reinterpret_cast<const uint32_t*>(P->d_signs);
+  sp.words32 = P->words64 * 2;
+  sp.K = P->d_K;
+  sp.r = P->r;
+  sp.n = P->n;
+  sp.J = P->J;
+  sp.log_j = P->log_j;
+  sp.n_sub = P->n_sub;
+  sp.S_act = P->S_act;
+  sp.groups = P->groups;
+  sp.scale = P->scale;
+  return sp;
+}
+
+srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_bytes, void* stream) {
+  if (sp.total_cols == 0) return SRHT_OK;
+  const size_t need = partial_bytes(P, sp.total_cols);
+  if (need) {
+    if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255)) return SRHT_EINVAL;
+    sp.partials = static_cast<float*>(ws);
+  }
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return SRHT_ECUDA;
+  if (dev != P->device) return SRHT_EINVAL;
+  cudaError_t e = srht::launch_sketch(P, sp, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* srht_status_str(srht_status s) {
+  switch (s) {
+    case SRHT_OK: return "SRHT_OK";
+    case SRHT_EINVAL: return "SRHT_EINVAL: invalid argument";
+    case SRHT_ENOMEM: return "SRHT_ENOMEM: device allocation failed";
+    case SRHT_ECUDA: return "SRHT_ECUDA: CUDA error";
+    case SRHT_EUNSUPPORTED: return "SRHT_EUNSUPPORTED: outside supported limits";
+  }
+  return "unknown srht_status";
+}
+
+srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t seed, int64_t batch,
+                                     srht_plan** out) {
+  if (!out) return SRHT_EINVAL;
+  *out = nullptr;
+  if (n < 1 || d < 0 || r < 1 || batch < 1 || batch > 65535) return SRHT_EINVAL;
+  int64_t N = 2;
+  while (N < n) N *= 2;
+  if (r > N) return SRHT_EINVAL;
+  if (N > (int64_t(1) << 30)) return SRHT_EUNSUPPORTED;
+
+  srht_plan* P = new (std::nothrow) srht_plan;
+  if (!P) return SRHT_ENOMEM;
+  std::memset(P, 0, sizeof(*P));
+  P->n = n;
+  P->d = d;
+  P->r = r;
+  P->N = N;
+  P->batch = batch;
+  P->seed = seed;
+  // Geometry (depends on n and r only).  Tile B ~ r (so ~1 sampled entry per
+  // tile row, Ailon-Liberty balance), clamped to [2^10, 2^14]; slabs of ~2^20 rows.
+  int lb = ceil_log2(r);
+  if (lb < 10) lb = 10;
+  if (lb > 14) lb = 14;
+  P->log_b = lb;
+  P->B = int64_t(1) << lb;
+  P->N_eff = N > P->B ? N : P->B;
+  const int64_t NB = P->N_eff / P->B;
+  int lj = 20 - lb;
+  if (lj < 0) lj = 0;
+  while ((int64_t(1) << lj) > NB) --lj;
+  P->log_j = lj;
+  P->J = int64_t(1) << lj;
+  P->n_sub = (n + P->B - 1) / P->B;
+  P->S_act = (P->n_sub + P->J - 1) / P->J;
+  P->threads = (int)(P->B / 32);
+  const int64_t per = (r + P->threads - 1) / P->threads;
+  P->rpt = per <= 4 ? 4 : per <= 8 ? 8 : per <= 16 ? 16 : 32;
+  P->groups = (r + (int64_t)P->rpt * P->threads - 1) / ((int64_t)P->rpt * P->threads);
+  P->words64 = P->N_eff / 64;
+  P->scale = (float)(1.0 / std::sqrt((double)r));
+  if (cudaGetDevice(&P->device) != cudaSuccess) {
+    delete P;
+    return SRHT_ECUDA;
+  }
+  if (cudaMalloc(&P->d_signs, (size_t)batch * P->words64 * sizeof(uint64_t)) != cudaSuccess) {
+    delete P;
+    return SRHT_ENOMEM;
+  }
+  if (cudaMalloc(&P->d_K, (size_t)batch * r * sizeof(int32_t)) != cudaSuccess) {
+    cudaFree(P->d_signs);
+    delete P;
+    return SRHT_ENOMEM;
+  }
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    srht_plan_destroy(P);
+    return SRHT_ECUDA;
+  }
+  const cudaError_t e = srht::build_plan_device(P, st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) {
+    srht_plan_destroy(P);
+    return e == cudaErrorMemoryAllocation ? SRHT_ENOMEM : SRHT_ECUDA;
+  }
+  *out = P;
+  return SRHT_OK;
+}
+
+srht_status srht_plan_create(int64_t n, int64_t d, int64_t r, uint64_t seed, srht_plan** out) {
+  return srht_plan_create_batched(n, d, r, seed, 1, out);
+}
+
+srht_status srht_plan_destroy(srht_plan* P) {
+  if (!P) return SRHT_OK;
+  cudaFree(P->d_signs);
+  cudaFree(P->d_K);
+  delete P;
+  return SRHT_OK;
+}
+
+srht_status srht_plan_info(const srht_plan* P, int64_t* N, int64_t* r, int64_t* batch) {
+  if (!P) return SRHT_EINVAL;
+  if (N) *N = P->N;
+  if (r) *r = P->r;
+  if (batch) *batch = P->batch;
+  return SRHT_OK;
+}
+
+srht_status srht_plan_copy_indices(const srht_plan* P, int64_t problem, int32_t* host_K) {
+  if (!P || !host_K || problem < 0 || problem >= P->batch) return SRHT_EINVAL;
+  return cudaMemcpy(host_K, P->d_K + problem * P->r, P->r * sizeof(int32_t), cudaMemcpyDeviceToHost) == cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
+srht_status srht_plan_copy_signs(const srht_plan* P, int64_t problem, uint64_t* host_words) {
+  if (!P || !host_words || problem < 0 || problem >= P->batch) return SRHT_EINVAL;
+  const int64_t w = (P->N + 63) / 64;
+  return cudaMemcpy(host_words, P->d_signs + problem * P->words64, w * sizeof(uint64_t), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
+size_t srht_workspace_bytes(const srht_plan* P, int64_t ncols) {
+  if (!P) return 0;
+  return partial_bytes(P, ncols);
+}
+
+srht_status srht_sketch_columns(const srht_plan* P, const srht_matrix* M, float* SM, int64_t ldsm, void* ws,
+                                size_t ws_bytes, void* stream) {
+  if (!P || !valid_matrix(M) || M->rows != P->n || ldsm < P->r) return SRHT_EINVAL;
+  if (M->cols > 0 && !SM) return SRHT_EINVAL;
+  srht::SketchParams sp = base_params(P);
+  sp.src[0] = make_src(M, SM, ldsm);
+  sp.ncols0 = M->cols;
+  sp.total_cols = M->cols;
+  sp.cols_per_problem = INT64_MAX;  // every column uses problem 0's plan
+  return run(P, sp, ws, ws_bytes, stream);
+}
+
+srht_status srht_sketch(const srht_plan* P, const srht_matrix* A, const srht_matrix* b, float* SA, int64_t ldsa,
+                        float* Sb, void* ws, size_t ws_bytes, void* stream) {
+  if (!P || !valid_matrix(A) || A->rows != P->n || ldsa < P->r) return SRHT_EINVAL;
+  if (A->cols > 0 && !SA) return SRHT_EINVAL;
+  if (b) {
+    if (!valid_matrix(b) || b->rows != P->n || b->cols != 1 || !Sb) return SRHT_EINVAL;
+  }
+  srht::SketchParams sp = base_params(P);
+  sp.src[0] = make_src(A, SA, ldsa);
+  sp.ncols0 = A->cols;
+  sp.total_cols = A->cols;
+  if (b) {
+    sp.src[1] = make_src(b, Sb, P->r);
+    sp.total_cols += 1;
+  }
+  sp.cols_per_problem = INT64_MAX;  // a single problem (p = 0)
+  return run(P, sp, ws, ws_bytes, stream);
+}
+
+srht_status srht_sketch_batched(const srht_plan* P, const srht_matrix* M, float* SM, void* ws, size_t ws_bytes,
+                                void* stream) {
+  if (!P || !valid_matrix(M) || M->rows != P->n || !SM) return SRHT_EINVAL;
+  if (M->cols % P->batch != 0 || M->cols == 0) return SRHT_EINVAL;
+  srht::SketchParams sp = base_params(P);
+  sp.src[0] = make_src(M, SM, P->r);
+  sp.ncols0 = M->cols;
+  sp.total_cols = M->cols;
+  sp.cols_per_problem = M->cols / P->batch;
+  return run(P, sp, ws, ws_bytes, stream);
+}
+
+srht_status srht_profile_set_events(void* before, void* after) {
+  srht::g_prof_before = static_cast<cudaEvent_t>(before);
+  srht::g_prof_after = static_cast<cudaEvent_t>(after);
+  return SRHT_OK;
+}
+
+srht_status srht_gen_uniform(uint64_t seed, uint64_t stream0, int64_t rows, int64_t cols, float* out, int64_t ld,
+                             void* stream) {
+  if (rows < 0 || cols < 0 || ld < rows || (rows > 0 && cols > 0 && !out)) return SRHT_EINVAL;
+  return srht::launch_gen_uniform(seed, stream0, rows, cols, out, ld, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
+// Host-buffer variant: stream column chunks host -> device, sketch, device -> host,
+// double-buffered over two streams so copies overlap the kernels.
+srht_status srht_sketch_columns_host(const srht_plan* P, const srht_matrix* Mh, float* SMh, int64_t ldsm) {
+  if (!P || !valid_matrix(Mh) || Mh->rows != P->n || ldsm < P->r) return SRHT_EINVAL;
+  if (Mh->cols == 0) return SRHT_OK;
+  if (!SMh) return SRHT_EINVAL;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != P->device) return SRHT_EINVAL;
+  const int64_t n = Mh->rows, ncols = Mh->cols;
+  // columns per chunk: ~256 MB of input, at least 1
+  int64_t chunk = 1;
+  if (Mh->fmt == SRHT_DENSE) {
+    const int64_t bytes_per_col = n * (int64_t)sizeof(float);
+    chunk = (int64_t(256) << 20) / (bytes_per_col > 0 ? bytes_per_col : 1);
+  } else {
+    const int64_t per = (Mh->nnz * 12) / (ncols > 0 ? ncols : 1) + 16;
+    chunk = (int64_t(256) << 20) / per;
+  }
+  if (chunk < 1) chunk = 1;
+  if (chunk > ncols) chunk = ncols;
+  // For CSC the largest chunk nnz bounds the buffer size.
+  int64_t max_nnz = 0;
+  if (Mh->fmt == SRHT_CSC) {
+    for (int64_t c0 = 0; c0 < ncols; c0 += chunk) {
+      const int64_t c1 = c0 + chunk < ncols ? c0 + chunk : ncols;
+      const int64_t z = Mh->colptr[c1] - Mh->colptr[c0];
+      if (z > max_nnz) max_nnz = z;
+    }
+  }
+  const size_t ws = partial_bytes(P, chunk);
+  struct Buf {
+    float* vals = nullptr;
+    int64_t* colptr = nullptr;
+    int32_t* rowidx = nullptr;
+    float* out = nullptr;
+    void* ws = nullptr;
+    cudaStream_t st = nullptr;
+  } buf[2];
+  srht_status status = SRHT_OK;
+  auto fail = [&](srht_status s) {
+    if (status == SRHT_OK) status = s;
+  };
+  for (int i = 0; i < 2 && status == SRHT_OK; ++i) {
+    if (cudaStreamCreateWithFlags(&buf[i].st, cudaStreamNonBlocking) != cudaSuccess) fail(SRHT_ECUDA);
+    const size_t vbytes = Mh->fmt == SRHT_DENSE ? (size_t)n * chunk * sizeof(float) : (size_t)(max_nnz + 1) * sizeof(float);
+    if (cudaMalloc(&buf[i].vals, vbytes) != cudaSuccess) fail(SRHT_ENOMEM);
+    if (Mh->fmt == SRHT_CSC) {
+      if (cudaMalloc(&buf[i].colptr, (chunk + 1) * sizeof(int64_t)) != cudaSuccess) fail(SRHT_ENOMEM);
+      if (cudaMalloc(&buf[i].rowidx, (max_nnz + 1) * sizeof(int32_t)) != cudaSuccess) fail(SRHT_ENOMEM);
+    }
+    if (cudaMalloc(&buf[i].out, (size_t)P->r * chunk * sizeof(float)) != cudaSuccess) fail(SRHT_ENOMEM);
+    if (ws && cudaMalloc(&buf[i].ws, ws) != cudaSuccess) fail(SRHT_ENOMEM);
+  }
+  int64_t it = 0;
+  for (int64_t c0 = 0; c0 < ncols && status == SRHT_OK; c0 += chunk, ++it) {
+    Buf& b = buf[it & 1];
+    const int64_t nc = c0 + chunk < ncols ? chunk : ncols - c0;
+    srht_matrix Md = *Mh;
+    Md.cols = nc;
+    if (Mh->fmt == SRHT_DENSE) {
+      if (cudaMemcpy2DAsync(b.vals, n * sizeof(float), Mh->vals + c0 * Mh->ld, Mh->ld * sizeof(float),
+                            n * sizeof(float), nc, cudaMemcpyHostToDevice, b.st) != cudaSuccess) {
+        fail(SRHT_ECUDA);
+        break;
+      }
+      Md.vals = b.vals;
+      Md.ld = n;
+    } else {
+      const int64_t z0 = Mh->colptr[c0], z1 = Mh->colptr[c0 + nc];
+      if (cudaMemcpyAsync(b.colptr, Mh->colptr + c0, (nc + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, b.st) !=
+              cudaSuccess ||
+          (z1 > z0 && cudaMemcpyAsync(b.rowidx, Mh->rowidx + z0, (z1 - z0) * sizeof(int32_t),
+                                      cudaMemcpyHostToDevice, b.st) != cudaSuccess) ||
+          (z1 > z0 && cudaMemcpyAsync(b.vals, Mh->vals + z0, (z1 - z0) * sizeof(float), cudaMemcpyHostToDevice,
+                                      b.st) != cudaSuccess)) {
+        fail(SRHT_ECUDA);
+        break;
+      }
+      // colptr entries are absolute offsets: rebase the value/index pointers.
+      Md.colptr = b.colptr;
+      Md.rowidx = b.rowidx - z0;
+      Md.vals = b.vals - z0;
+      Md.nnz = z1 - z0;
+    }
+    const srht_status s = srht_sketch_columns(P, &Md, b.out, P->r, b.ws, ws, b.st);
+    if (s != SRHT_OK) {
+      fail(s);
+      break;
+    }
+    if (cudaMemcpy2DAsync(SMh + c0 * ldsm, ldsm * sizeof(float), b.out, P->r * sizeof(float), P->r * sizeof(float),
+                          nc, cudaMemcpyDeviceToHost, b.st) != cudaSuccess) {
+      fail(SRHT_ECUDA);
+      break;
+    }
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (buf[i].st && cudaStreamSynchronize(buf[i].st) != cudaSuccess) fail(SRHT_ECUDA);
+  }
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(buf[i].vals);
+    cudaFree(buf[i].colptr);
+    cudaFree(buf[i].rowidx);
+    cudaFree(buf[i].out);
+    cudaFree(buf[i].ws);
+    if (buf[i].st) cudaStreamDestroy(buf[i].st);
+  }
+  return status;
+}
+
+}  // extern "C"

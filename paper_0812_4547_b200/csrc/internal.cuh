@@ -1,0 +1,73 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/srht.h"
+
+struct srht_plan {
+  int64_t n, d, r, N, batch;
+  uint64_t seed;
+  // Tile / slab geometry: depends on (n, r) only.
+  int log_b;        // tile bits; B = 2^log_b rows per sub-block
+  int64_t B;
+  int64_t N_eff;    // max(N, B)
+  int log_j;        // sub-blocks per slab J = 2^log_j
+  int64_t J;
+  int64_t n_sub;    // sub-blocks holding rows < n: ceil(n / B)
+  int64_t S_act;    // slabs holding rows < n: ceil(n_sub / J)
+  int threads;      // CTA size = B / 32
+  int rpt;          // accumulators per thread
+  int64_t groups;   // sample groups = ceil(r / (rpt * threads))
+  int64_t words64;  // sign words per problem = N_eff / 64
+  float scale;      // r^{-1/2} rounded to FP32
+  int device;
+  uint64_t* d_signs;  // [batch][words64]
+  int32_t* d_K;       // [batch][r], ascending
+};
+
+namespace srht {
+
+// Plan builder (plan.cu): fills d_signs and d_K; synchronous on `stream`.
+cudaError_t build_plan_device(srht_plan* P, cudaStream_t stream);
+
+// One column source of a sketch launch.
+struct ColSrc {
+  int fmt;                // SRHT_DENSE / SRHT_CSC
+  int vec;                // dense: 16-byte vector loads allowed
+  const float* vals;
+  int64_t ld;
+  const int64_t* colptr;
+  const int32_t* rowidx;
+  int64_t ncols;
+  float* out;             // column j of this source -> out + j * ldo
+  int64_t ldo;
+};
+
+struct SketchParams {
+  ColSrc src[2];
+  int64_t ncols0;             // columns of src[0]; src[1] follows
+  int64_t total_cols;
+  int64_t cols_per_problem;   // problem of global column g = g / cols_per_problem
+  const uint32_t* signs;      // sign words viewed as uint32
+  int64_t words32;            // per problem
+  const int32_t* K;
+  int64_t r;
+  int64_t n;
+  int64_t J;
+  int log_j;
+  int64_t n_sub;
+  int64_t S_act;
+  int64_t groups;
+  float scale;
+  float* partials;            // [S_act][total_cols][r] when S_act > 1
+};
+
+cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream_t stream);
+
+extern cudaEvent_t g_prof_before, g_prof_after;  // srht_profile_set_events
+
+cudaError_t launch_gen_uniform(uint64_t seed, uint64_t stream0, int64_t rows, int64_t cols,
+                               float* out, int64_t ld, cudaStream_t stream);
+
+}  // namespace srht

@@ -1,0 +1,349 @@
+// SRHT sketch kernels for sm_100a.
+//
+// Output (Algorithm 1 step 5 inputs; Phi of P:461-465):
+//   SM[t, j] = r^{-1/2} * sum_{i<n} (-1)^{popc(k_t & i)} sigma_i M[i, j].
+//
+// Decomposition (Ailon-Liberty-style pruning).  Split a row index
+// i = (i_slab, i_mid, i_lo) with i_lo the low b bits (tile of B = 2^b rows),
+// i_mid the next log J bits (sub-block inside a slab) and i_slab the rest; the
+// same split of a kept row k gives (k_slab, k_mid, k_lo).  Because
+// popc(k & i) = popc(k_lo & i_lo) + popc(k_mid & i_mid) + popc(k_slab & i_slab),
+//
+//   SM[t] = r^{-1/2} sum_s (-1)^{popc(k_slab & s)}
+//                      sum_j (-1)^{popc(k_mid & j)} (H_B D x_{s,j})[k_lo],
+//
+// so a CTA streams the sub-blocks x_{s,j} of one (column, slab), transforms
+// each tile completely on chip (z = H_B D x, b stages), and accumulates only
+// the r sampled entries z[k_lo(t)] with the k_mid sign: ~b + r/B adds per
+// element instead of log2 N.  The slab sum (k_slab signs, r^{-1/2}) is done by
+// k_reduce_slabs in a fixed order, so results do not depend on how columns are
+// split across launches or GPUs.
+//
+// In-tile FWHT of B = 2^b FP32 values by T = B/32 threads, 32 values each,
+// in 2-3 rounds of up to 5 bits (registers) with XOR-swizzled shared-memory
+// exchanges in between; butterflies use packed FADD2/FFMA2 (sm_100).
+#include <cuda_runtime.h>
+
+#include "internal.cuh"
+
+namespace srht {
+namespace {
+
+// Bank-conflict-free swizzle of the tile: word x lives at phys(x).  It is
+// linear over GF(2), so phys(base | off) = phys(base) ^ phys(off).
+__host__ __device__ constexpr int phys(int x) { return x ^ ((x >> 5) & 31); }
+
+// Round 2 register bit k (LOG_B > 10): bits 7.. are transformed, the rest fill.
+__host__ __device__ constexpr int reg2_bit(int LOG_B, int k) {
+  return k < LOG_B - 10 ? 7 + k
+                        : (k - (LOG_B - 10) == 0   ? LOG_B - 3
+                           : k - (LOG_B - 10) == 1 ? LOG_B - 2
+                           : k - (LOG_B - 10) == 2 ? LOG_B - 1
+                           : k - (LOG_B - 10) == 3 ? 6
+                                                   : 5);
+}
+
+template <int LOG_B>
+__host__ __device__ constexpr int off0(int u) {  // round 0: bits {0,1,b-3,b-2,b-1}
+  return (u & 3) | ((u >> 2) << (LOG_B - 3));
+}
+__host__ __device__ constexpr int off1(int u) { return u << 2; }  // round 1: bits 2..6
+template <int LOG_B>
+__host__ __device__ constexpr int off2(int u) {
+  return (((u >> 0) & 1) << reg2_bit(LOG_B, 0)) | (((u >> 1) & 1) << reg2_bit(LOG_B, 1)) |
+         (((u >> 2) & 1) << reg2_bit(LOG_B, 2)) | (((u >> 3) & 1) << reg2_bit(LOG_B, 3)) |
+         (((u >> 4) & 1) << reg2_bit(LOG_B, 4));
+}
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+
+// Unnormalized Walsh-Hadamard butterflies over the low NB bits of the register
+// index u (value u lives in v[u >> 1].x / .y).  Natural order: (a, b) -> (a+b, a-b).
+template <int NB>
+__device__ __forceinline__ void fwht_regs(float2 (&v)[16]) {
+  if constexpr (NB >= 1) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m)  // within-pair bit: one FFMA2 per pair
+      v[m] = __ffma2_rn(v[m], make_float2(1.f, -1.f), make_float2(v[m].y, v[m].x));
+  }
+#pragma unroll
+  for (int s = 1; s < NB; ++s) {
+    const int st = 1 << (s - 1);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      if (!(m & st)) {
+        const float2 a = v[m], b = v[m | st];
+        v[m] = add2(a, b);
+        v[m | st] = sub2(a, b);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float flip(float x, uint32_t bit) {
+  return __uint_as_float(__float_as_uint(x) ^ (bit << 31));
+}
+
+template <int LOG_B, int RPT>
+__global__ void __launch_bounds__((1 << LOG_B) / 32, 512 / ((1 << LOG_B) / 32))
+    k_sketch_tiles(const __grid_constant__ SketchParams P) {
+  constexpr int B = 1 << LOG_B;
+  constexpr int T = B / 32;
+  extern __shared__ __align__(16) float tile[];
+  __shared__ int64_t s_ptr;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- decode the work item: (column, slab, sample group) ----
+  int64_t item = blockIdx.x;
+  const int64_t g = item % P.groups;
+  item /= P.groups;
+  const int64_t s = item % P.S_act;
+  const int64_t col = item / P.S_act;
+  const bool second = col >= P.ncols0;
+  const ColSrc& cs = second ? P.src[1] : P.src[0];
+  const int64_t lc = second ? col - P.ncols0 : col;
+  const int64_t prob = col / P.cols_per_problem;
+  const uint32_t* __restrict__ signs = P.signs + prob * P.words32;
+  const int32_t* __restrict__ Kp = P.K + prob * P.r;
+
+  // ---- per-thread bases of the three exchange layouts (swizzled) ----
+  const int pb0 = phys((lane << 2) | (warp << 7));
+  const int pb1 = phys((lane & 3) | ((lane >> 2) << 7) | (warp << 10));
+  int b2 = lane;
+  {
+    int w = warp, k = 0;
+    for (int bit = 5; bit < LOG_B; ++bit) {
+      bool is_reg = false;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) is_reg |= (reg2_bit(LOG_B, q) == bit);
+      if (LOG_B > 10 && !is_reg) {
+        b2 |= ((w >> k) & 1) << bit;
+        ++k;
+      }
+    }
+  }
+  const int pb2 = phys(b2);
+
+  // ---- sample metadata: byte offset of phys(k_lo) | k_mid << 16 ----
+  uint32_t meta[RPT];
+  float acc[RPT];
+  const int64_t t0 = g * (int64_t)RPT * T;
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int64_t t = t0 + (int64_t)q * T + tid;
+    uint32_t m = 0;
+    if (t < P.r) {
+      const int32_t k = Kp[t];
+      const int lo = k & (B - 1);
+      const uint32_t mid = (uint32_t)(k >> LOG_B) & (uint32_t)(P.J - 1);
+      m = ((uint32_t)phys(lo) << 2) | (mid << 16);
+    }
+    meta[q] = m;
+    acc[q] = 0.f;
+  }
+
+  const int64_t j0 = s * P.J;
+  const int64_t j1 = (j0 + P.J < P.n_sub) ? j0 + P.J : P.n_sub;
+  const int64_t n = P.n;
+
+  int64_t cptr = 0, cend = 0;
+  if (cs.fmt == SRHT_CSC) {
+    cend = cs.colptr[lc + 1];
+    if (tid == 0) {
+      int64_t lo = cs.colptr[lc], hi = cend;
+      const int64_t target = j0 * (int64_t)B;
+      while (lo < hi) {  // lower_bound(rowidx, target)
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)cs.rowidx[mid] < target) lo = mid + 1; else hi = mid;
+      }
+      s_ptr = lo;
+    }
+    __syncthreads();
+    cptr = s_ptr;
+  }
+
+  for (int64_t j = j0; j < j1; ++j) {
+    const int64_t row0 = j * (int64_t)B;
+    float2 v[16];
+    // ---- round 0: load D x (bits 0,1 and the top three bits in registers) ----
+    if (cs.fmt == SRHT_DENSE) {
+      const float* __restrict__ colp = cs.vals + lc * cs.ld;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const int64_t row = row0 + ((lane << 2) | (warp << 7) | (h << (LOG_B - 3)));
+        float4 f;
+        if (cs.vec && row + 3 < n) {
+          f = __ldcs(reinterpret_cast<const float4*>(colp + row));
+        } else {
+          f.x = row + 0 < n ? colp[row + 0] : 0.f;
+          f.y = row + 1 < n ? colp[row + 1] : 0.f;
+          f.z = row + 2 < n ? colp[row + 2] : 0.f;
+          f.w = row + 3 < n ? colp[row + 3] : 0.f;
+        }
+        const uint32_t sw = __ldg(signs + (row >> 5)) >> (row & 31);
+        v[2 * h] = make_float2(flip(f.x, sw & 1u), flip(f.y, (sw >> 1) & 1u));
+        v[2 * h + 1] = make_float2(flip(f.z, (sw >> 2) & 1u), flip(f.w, (sw >> 3) & 1u));
+      }
+    } else {
+      // CSC: densify the sub-block into the tile (signs applied), then read it.
+#pragma unroll
+      for (int i = tid; i < B / 4; i += T) reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncthreads();
+      const int64_t rowend = row0 + B;
+      while (true) {
+        const int64_t e = cptr + tid;
+        bool in = false;
+        if (e < cend) {
+          const int64_t row = cs.rowidx[e];
+          if (row < rowend) {
+            in = true;
+            const uint32_t sb = (__ldg(signs + (row >> 5)) >> (row & 31)) & 1u;
+            atomicAdd(&tile[phys((int)(row - row0))], flip(cs.vals[e], sb));
+          }
+        }
+        const int cnt = __syncthreads_count(in);
+        cptr += cnt;
+        if (cnt < T) break;
+      }
+#pragma unroll
+      for (int u = 0; u < 32; u += 2) v[u >> 1] = make_float2(tile[pb0 ^ phys(off0<LOG_B>(u))],
+                                                             tile[pb0 ^ phys(off0<LOG_B>(u + 1))]);
+    }
+    fwht_regs<5>(v);
+#pragma unroll
+    for (int u = 0; u < 32; u += 2) {
+      tile[pb0 ^ phys(off0<LOG_B>(u))] = v[u >> 1].x;
+      tile[pb0 ^ phys(off0<LOG_B>(u + 1))] = v[u >> 1].y;
+    }
+    __syncthreads();
+    // ---- round 1: bits 2..6 ----
+#pragma unroll
+    for (int u = 0; u < 32; u += 2)
+      v[u >> 1] = make_float2(tile[pb1 ^ phys(off1(u))], tile[pb1 ^ phys(off1(u + 1))]);
+    fwht_regs<5>(v);
+#pragma unroll
+    for (int u = 0; u < 32; u += 2) {
+      tile[pb1 ^ phys(off1(u))] = v[u >> 1].x;
+      tile[pb1 ^ phys(off1(u + 1))] = v[u >> 1].y;
+    }
+    __syncthreads();
+    // ---- round 2: bits 7 .. b-4 ----
+    if constexpr (LOG_B > 10) {
+#pragma unroll
+      for (int u = 0; u < 32; u += 2)
+        v[u >> 1] = make_float2(tile[pb2 ^ phys(off2<LOG_B>(u))], tile[pb2 ^ phys(off2<LOG_B>(u + 1))]);
+      fwht_regs<LOG_B - 10>(v);
+#pragma unroll
+      for (int u = 0; u < 32; u += 2) {
+        tile[pb2 ^ phys(off2<LOG_B>(u))] = v[u >> 1].x;
+        tile[pb2 ^ phys(off2<LOG_B>(u + 1))] = v[u >> 1].y;
+      }
+      __syncthreads();
+    }
+    // ---- pruned accumulate: acc_t += (-1)^{popc(k_mid & j)} z[k_lo] ----
+    const uint32_t jl = (uint32_t)(j - j0);
+    const char* tb = reinterpret_cast<const char*>(tile);
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const uint32_t m = meta[q];
+      const float z = *reinterpret_cast<const float*>(tb + (m & 0xffffu));
+      acc[q] += flip(z, __popc((m >> 16) & jl) & 1u);
+    }
+    __syncthreads();
+  }
+
+  // ---- epilogue ----
+  if (P.S_act == 1) {
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int64_t t = t0 + (int64_t)q * T + tid;
+      if (t < P.r) cs.out[lc * cs.ldo + t] = acc[q] * P.scale;
+    }
+  } else {
+    float* __restrict__ part = P.partials + (s * P.total_cols + col) * P.r;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int64_t t = t0 + (int64_t)q * T + tid;
+      if (t < P.r) part[t] = acc[q];
+    }
+  }
+}
+
+// Fixed-order signed sum over slabs, scale, and write (one thread per output).
+__global__ void k_reduce_slabs(const __grid_constant__ SketchParams P, int slab_shift) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t col = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  if (t >= P.r || col >= P.total_cols) return;
+  const int64_t prob = col / P.cols_per_problem;
+  const uint32_t ks = (uint32_t)(P.K[prob * P.r + t] >> slab_shift);
+  float sum = 0.f;
+  for (int64_t s = 0; s < P.S_act; ++s) {
+    const float v = P.partials[(s * P.total_cols + col) * P.r + t];
+    sum += flip(v, __popc(ks & (uint32_t)s) & 1u);
+  }
+  const bool second = col >= P.ncols0;
+  const ColSrc& cs = second ? P.src[1] : P.src[0];
+  const int64_t lc = second ? col - P.ncols0 : col;
+  cs.out[lc * cs.ldo + t] = sum * P.scale;
+}
+
+template <int LOG_B, int RPT>
+cudaError_t launch_t(const SketchParams& sp, int64_t items, cudaStream_t stream) {
+  constexpr int B = 1 << LOG_B;
+  const size_t smem = (size_t)B * sizeof(float);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(k_sketch_tiles<LOG_B, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  for (int64_t done = 0; done < items;) {
+    // one launch covers at most 2^31-1 items (never reached in practice)
+    const int64_t cnt = items - done < 0x7fffffff ? items - done : 0x7fffffff;
+    k_sketch_tiles<LOG_B, RPT><<<(unsigned)cnt, B / 32, smem, stream>>>(sp);
+    done += cnt;
+  }
+  return cudaGetLastError();
+}
+
+template <int LOG_B>
+cudaError_t launch_b(int rpt, const SketchParams& sp, int64_t items, cudaStream_t stream) {
+  switch (rpt) {
+    case 4: return launch_t<LOG_B, 4>(sp, items, stream);
+    case 8: return launch_t<LOG_B, 8>(sp, items, stream);
+    case 16: return launch_t<LOG_B, 16>(sp, items, stream);
+    case 32: return launch_t<LOG_B, 32>(sp, items, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+cudaEvent_t g_prof_before = nullptr, g_prof_after = nullptr;
+
+cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream_t stream) {
+  if (sp.total_cols <= 0) return cudaSuccess;
+  const int64_t items = sp.total_cols * sp.S_act * sp.groups;
+  cudaError_t e;
+  if (g_prof_before) cudaEventRecord(g_prof_before, stream);
+  switch (P->log_b) {
+    case 10: e = launch_b<10>(P->rpt, sp, items, stream); break;
+    case 11: e = launch_b<11>(P->rpt, sp, items, stream); break;
+    case 12: e = launch_b<12>(P->rpt, sp, items, stream); break;
+    case 13: e = launch_b<13>(P->rpt, sp, items, stream); break;
+    case 14: e = launch_b<14>(P->rpt, sp, items, stream); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (g_prof_after) cudaEventRecord(g_prof_after, stream);
+  if (e != cudaSuccess || sp.S_act == 1) return e;
+  const int64_t zc = (sp.total_cols + 65534) / 65535;
+  dim3 grid((unsigned)((sp.r + 255) / 256), (unsigned)(sp.total_cols < 65535 ? sp.total_cols : 65535),
+            (unsigned)zc);
+  k_reduce_slabs<<<grid, 256, 0, stream>>>(sp, P->log_b + P->log_j);
+  return cudaGetLastError();
+}
+
+}  // namespace srht

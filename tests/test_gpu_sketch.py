@@ -1,0 +1,221 @@
+"""GPU sketch vs oracle, element by element (through the C ABI)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import torch
+    import paper_0812_4547_b200 as m
+    torch.cuda.init()
+    return m
+
+
+def to_dev(M):
+    import torch
+    t = torch.from_numpy(np.asfortranarray(M, dtype=np.float32))
+    return t.t().contiguous().t().cuda() if t.dim() == 2 else t.cuda()
+
+
+def tol(M, n):
+    """north_star: |gpu - oracle| <= 1e-5 * sqrt(n) * max|col| (R11: n original, per column)."""
+    return 1e-5 * math.sqrt(n) * np.max(np.abs(M), axis=0)
+
+
+def check_close(got, ref, M):
+    got = np.asarray(got, dtype=np.float64)
+    bound = tol(M, M.shape[0])
+    err = np.abs(got - ref)
+    assert np.all(err <= bound[None, :] + 1e-30), (err.max(), (err / np.maximum(bound, 1e-30)).max())
+    return (err / np.maximum(bound, 1e-30)).max()
+
+
+@pytest.mark.parametrize("n,c,r,seed", [
+    (4096, 17, 256, 0),        # config 1 shape
+    (1000, 3, 100, 1),         # ragged tail, r not a power of two
+    (5, 2, 3, 2),              # tiny n (N = 8 < tile)
+    (1, 1, 1, 3),              # n = 1
+    (10000, 4, 350, 4),        # paper Section 4.2 shape class (n = 10,000 -> N = 16384)
+    (33333, 5, 1500, 5),       # several tiles + ragged
+    (1 << 17, 3, 4096, 6),     # multi sub-block, single slab
+    (300000, 2, 2000, 7),      # several slabs (partials + reduce)
+    (3 << 19, 2, 8192, 8),     # several slabs, B = 2^13
+    (1 << 21, 2, 16384, 9),    # B = 2^14, two slabs
+    (70000, 2, 20000, 10),     # r > 32 * threads: several sample groups
+])
+def test_dense_random_parity(lib, n, c, r, seed):
+    from oracle import srht as osr
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, c)).astype(np.float32)
+    plan = lib.Plan(n, c - 1, r, seed)
+    SM = plan.sketch_columns(to_dev(M)).cpu().numpy()
+    ref = osr.sketch(M.astype(np.float64), seed, r)
+    check_close(SM, ref, M)
+
+
+@pytest.mark.parametrize("n,r", [(4096, 256), (1 << 16, 1024), (1 << 18, 4096), (1 << 20, 16384), (50000, 1024)])
+def test_integer_inputs_bit_exact(lib, n, r):
+    # Integer inputs with n * max|a| < 2^24 make every partial sum exact in FP32
+    # under any summation order, and r = 4^j makes r^{-1/2} a power of two, so
+    # the GPU result must equal the oracle's exactly.
+    from oracle import srht as osr
+    rng = np.random.default_rng(n)
+    amax = max(1, (1 << 23) // n)
+    M = rng.integers(-amax, amax + 1, size=(n, 3)).astype(np.float32)
+    plan = lib.Plan(n, 2, r, 11)
+    SM = plan.sketch_columns(to_dev(M)).cpu().numpy().astype(np.float64)
+    ref = osr.sketch(M.astype(np.float64), 11, r)
+    assert np.array_equal(SM, ref)
+
+
+def test_single_nonzero_closed_form(lib):
+    from oracle import srht as osr
+    n, r, seed = 20000, 1024, 3
+    N = osr.padded_size(n)
+    rows = [0, 1, 31, 4095, 12345, n - 1]
+    M = np.zeros((n, len(rows)), dtype=np.float32)
+    for j, i in enumerate(rows):
+        M[i, j] = 1.0
+    plan = lib.Plan(n, 0, r, seed)
+    SM = plan.sketch_columns(to_dev(M)).cpu().numpy()
+    sig = osr.plan_signs(seed, 0, N)
+    K = osr.plan_samples(seed, 0, N, r)
+    for j, i in enumerate(rows):
+        expect = np.array([sig[i] * (-1.0) ** bin(int(k) & i).count("1") for k in K]) / 32.0
+        assert np.array_equal(SM[:, j].astype(np.float64), expect)
+
+
+def test_sketch_A_b_matches_columns(lib):
+    import torch
+    n, d, r = 30000, 6, 512
+    M, _ = workloads.dense_host(n, d, seed=4)
+    plan = lib.Plan(n, d, r, 4)
+    Md = to_dev(M)
+    SA, Sb = plan.sketch(Md[:, :d], Md[:, d])
+    SM = plan.sketch_columns(Md)
+    torch.cuda.synchronize()
+    assert torch.equal(SA, SM[:, :d]) and torch.equal(Sb, SM[:, d])
+
+
+def test_column_shards_bit_identical(lib):
+    import torch
+    n, c, r = 1 << 19, 13, 4096
+    M = np.random.default_rng(0).random((n, c), dtype=np.float32)
+    plan = lib.Plan(n, c - 1, r, 1)
+    Md = to_dev(M)
+    full = plan.sketch_columns(Md)
+    parts = [plan.sketch_columns(Md[:, a:b]) for a, b in [(0, 5), (5, 6), (6, 13)]]
+    assert torch.equal(full, torch.cat(parts, dim=1))
+
+
+def test_ld_greater_than_n_and_unaligned(lib):
+    import torch
+    from oracle import srht as osr
+    n, c, r = 5003, 3, 200
+    rng = np.random.default_rng(2)
+    big = torch.from_numpy(rng.standard_normal((5011, c + 1)).astype(np.float32)).t().contiguous().t().cuda()
+    view = big[3:3 + n, 1:]  # ld = 5011, base pointer not 16-byte aligned
+    plan = lib.Plan(n, c - 1, r, 2)
+    SM = plan.sketch_columns(view).cpu().numpy()
+    Mh = view.cpu().numpy()
+    check_close(SM, osr.sketch(Mh.astype(np.float64), 2, r), Mh)
+
+
+def _csc_dev(colptr, rowidx, vals, shape):
+    import torch
+    return lib_csc(torch.from_numpy(np.asarray(colptr, dtype=np.int64)).cuda(),
+                   torch.from_numpy(np.asarray(rowidx, dtype=np.int32)).cuda(),
+                   torch.from_numpy(np.asarray(vals, dtype=np.float32)).cuda(), shape)
+
+
+def lib_csc(*a):
+    import paper_0812_4547_b200 as m
+    return m.CSC(*a)
+
+
+@pytest.mark.parametrize("n,ncols,per,r", [(8192, 12, 164, 1024), (1 << 17, 5, 1311, 4096), (3000, 4, 40, 64),
+                                           (300000, 3, 3000, 2048)])
+def test_csc_parity(lib, n, ncols, per, r):
+    from oracle import srht as osr
+    colptr, rowidx, vals = workloads.csc_lognormal(1, n, ncols, per)
+    dense = workloads.csc_to_dense(colptr, rowidx, vals, n, ncols)
+    plan = lib.Plan(n, ncols - 1, r, 5)
+    SM = plan.sketch_columns(_csc_dev(colptr, rowidx, vals, (n, ncols))).cpu().numpy()
+    check_close(SM, osr.sketch(dense, 5, r), dense.astype(np.float32))
+
+
+def test_csc_empty_and_duplicate_columns(lib):
+    from oracle import srht as osr
+    n, r = 5000, 300
+    # col0: empty; col1: duplicates of row 7 (summed) and rows at the tile edges; col2: one entry at n-1
+    colptr = np.array([0, 0, 6, 7], dtype=np.int64)
+    rowidx = np.array([7, 7, 1023, 1024, 2047, 4999, 4999], dtype=np.int32)
+    vals = np.array([1.5, 2.5, -1.0, 3.0, 0.25, 4.0, -2.0], dtype=np.float32)
+    dense = workloads.csc_to_dense(colptr, rowidx, vals, n, 3)
+    plan = lib.Plan(n, 2, r, 9)
+    SM = plan.sketch_columns(_csc_dev(colptr, rowidx, vals, (n, 3))).cpu().numpy()
+    assert np.all(SM[:, 0] == 0)
+    check_close(SM, osr.sketch(dense, 9, r), dense.astype(np.float32) + 1e-30)
+
+
+def test_mixed_csc_A_dense_b(lib):
+    import torch
+    from oracle import srht as osr
+    w = workloads.config3_host(n=1 << 15, d=20)
+    n, d, r = w["n"], w["d"], 2048
+    plan = lib.Plan(n, d, r, 0)
+    A = _csc_dev(w["colptr"], w["rowidx"], w["vals"], (n, d))
+    SA, Sb = plan.sketch(A, torch.from_numpy(w["b"]).cuda())
+    dense = workloads.csc_to_dense(w["colptr"], w["rowidx"], w["vals"], n, d)
+    M = np.column_stack([dense, w["b"].astype(np.float64)])
+    ref = osr.sketch(M, 0, r)
+    got = np.column_stack([SA.cpu().numpy(), Sb.cpu().numpy()])
+    check_close(got, ref, M.astype(np.float32))
+
+
+def test_batched_dense_parity(lib):
+    from oracle import srht as osr
+    batch, n, c, r = 7, 3000, 4, 256
+    rng = np.random.default_rng(3)
+    M = rng.random((n, batch * c), dtype=np.float32)
+    plan = lib.Plan(n, c - 1, r, 13, batch=batch)
+    out = plan.sketch_batched(to_dev(M)).cpu().numpy()  # (batch, c, r)
+    for p in range(batch):
+        ref = osr.sketch(M[:, p * c:(p + 1) * c].astype(np.float64), 13, r, p=p)
+        check_close(out[p].T, ref, M[:, p * c:(p + 1) * c])
+
+
+def test_batched_csc_parity_small(lib):
+    from oracle import srht as osr
+    w = workloads.config2_host(batch=20, n=8192, d=10)
+    n, c, r = w["n"], w["d"] + 1, w["r"]
+    plan = lib.Plan(n, w["d"], r, 0, batch=w["batch"])
+    out = plan.sketch_batched(_csc_dev(w["colptr"], w["rowidx"], w["vals"], (n, w["batch"] * c))).cpu().numpy()
+    dense = workloads.csc_to_dense(w["colptr"], w["rowidx"], w["vals"], n, w["batch"] * c)
+    for p in range(w["batch"]):
+        blk = dense[:, p * c:(p + 1) * c]
+        check_close(out[p].T, osr.sketch(blk, 0, r, p=p), blk.astype(np.float32))
+
+
+def test_host_buffer_call_matches_device(lib):
+    import torch
+    n, c, r = 1 << 20, 9, 8192
+    M = torch.rand((c, n), dtype=torch.float32).t()
+    plan = lib.Plan(n, c - 1, r, 0)
+    dev = plan.sketch_columns(M.t().contiguous().t().cuda()).cpu()
+    host = plan.sketch_columns_host(M.t().contiguous().pin_memory().t())
+    assert torch.equal(dev, host)
+
+
+def test_invalid_sketch_arguments(lib):
+    import torch
+    plan = lib.Plan(100, 1, 10, 0)
+    with pytest.raises(lib.SrhtError):
+        plan.sketch_columns(torch.zeros((99, 2), device="cuda").t().contiguous().t())
