@@ -17,6 +17,7 @@ stream between barriers + synchronize, max over ranks; rank 0 prints one JSON li
 """
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -280,24 +281,24 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # per-step events around the tile kernel (library profiling hook)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        _lib.check(lib.srht_profile_start(args.steps), "srht_profile_start")
         ev0.record(stream)
         for i in range(args.steps):
-            lib.srht_profile_set_events(kev[i][0].cuda_event, kev[i][1].cuda_event)
             step()
         ev1.record(stream)
-        lib.srht_profile_set_events(None, None)
         torch.cuda.synchronize()
+        kms_arr = (ctypes.c_float * args.steps)()
+        kcount = ctypes.c_int()
+        _lib.check(lib.srht_profile_stop(kms_arr, args.steps, ctypes.byref(kcount)), "srht_profile_stop")
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    kms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    kms = statistics.mean(kms_arr[i] for i in range(kcount.value))
     t = torch.tensor([ms, kms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

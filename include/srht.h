@@ -146,13 +146,17 @@ srht_status srht_sketch_columns_host(const srht_plan* plan,
 
 const char* srht_status_str(srht_status s);
 
-/* ---- Profiling hook (benchmark instrumentation) ----
- * When set, every subsequent srht_sketch* call records `before` and `after`
- * (cudaEvent_t passed as void*) on its stream immediately around the main
- * tile kernel (k_sketch_tiles), so its duration can be timed with CUDA events
- * on the stream it runs on.  Pass NULL, NULL to clear.  Process-global, not
- * thread-safe; events must belong to the plan's device.                       */
-srht_status srht_profile_set_events(void* before, void* after);
+/* ---- Profiling (benchmark instrumentation) ----
+ * srht_profile_start(capacity): from now on, every srht_sketch* call records a
+ * pair of CUDA events on its own stream immediately around the main tile
+ * kernel (k_sketch_tiles), for up to `capacity` calls (later calls are not
+ * recorded).  srht_profile_stop(ms, capacity, &count): waits for the recorded
+ * events, writes the per-call tile-kernel durations in milliseconds to host
+ * array `ms` (up to `capacity` values), sets *count, frees the events and
+ * disables recording.  Process-global and not thread-safe; EINVAL if
+ * start is called twice without stop or capacity < 1.                        */
+srht_status srht_profile_start(int capacity);
+srht_status srht_profile_stop(float* ms, int capacity, int* count);
 
 /* ---- Workload generator (benchmark / test input only; not the method) ----
  * out[i + j*ld] = (word i of stream (seed, 2^32 + stream0 + j) >> 40) * 2^-24,

@@ -49,7 +49,8 @@ SIGNATURES = [
     ("srht_sketch_columns_host", ctypes.c_int, [_P, _MP, _P, _I64]),
     ("srht_status_str", ctypes.c_char_p, [ctypes.c_int]),
     ("srht_gen_uniform", ctypes.c_int, [_U64, _U64, _I64, _I64, _P, _I64, _P]),
-    ("srht_profile_set_events", ctypes.c_int, [_P, _P]),
+    ("srht_profile_start", ctypes.c_int, [ctypes.c_int]),
+    ("srht_profile_stop", ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
 ]
 
 _lib = None

@@ -50,9 +50,62 @@ srht::ColSrc make_src(const srht_matrix* M, float* out, int64_t ldo) {
 }
 
 size_t partial_bytes(const srht_plan* P, int64_t ncols) {
-  if (P->S_act <= 1 || ncols <= 0) return 0;
-  const size_t b = (size_t)P->S_act * (size_t)ncols * (size_t)P->r * sizeof(float);
+  if (ncols <= 0) return 0;
+  int64_t S = P->S_act > 1 ? P->S_act : 0;
+  if (P->ws_ok && P->S_act2 > 1 && P->S_act2 > S) S = P->S_act2;
+  if (S <= 1) return 0;
+  const size_t b = (size_t)S * (size_t)ncols * (size_t)P->r * sizeof(float);
   return (b + 255) & ~size_t(255);
+}
+
+// Kernel v2 consumer slot layout (host side, once per plan).  Sample t goes to
+// slot (q, c): consumer thread c = 32*w + lane reads meta[q*256 + c].  Rows
+// (q, w) of 32 lanes take at most one sample per shared-memory bank of
+// phys(k_lo) where possible, so the gather LDS is conflict-free.
+cudaError_t build_ws_layout(srht_plan* P) {
+  const int64_t r = P->r;
+  const int rows = P->rpt2 * 8;
+  const int slots = P->rpt2 * 256;
+  std::vector<int32_t> K(r);
+  cudaError_t e = cudaMemcpy(K.data(), P->d_K, r * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return e;
+  std::vector<std::vector<int32_t>> bucket(32);
+  for (int64_t t = 0; t < r; ++t) {
+    const int lo = K[t] & ((1 << 14) - 1);
+    bucket[srht::ws_phys(lo) & 31].push_back((int32_t)t);
+  }
+  std::vector<int32_t> slot_t(slots, -1);
+  std::vector<size_t> head(32, 0);
+  for (int row = 0; row < rows; ++row)
+    for (int b = 0; b < 32; ++b)
+      if (head[b] < bucket[b].size()) slot_t[row * 32 + b] = bucket[b][head[b]++];
+  int free_pos = 0;
+  for (int b = 0; b < 32; ++b)
+    while (head[b] < bucket[b].size()) {
+      while (slot_t[free_pos] >= 0) ++free_pos;
+      slot_t[free_pos] = bucket[b][head[b]++];
+    }
+  // row = q*8 + w, lane = bank  ->  meta index q*256 + 32*w + lane
+  std::vector<uint32_t> meta(slots, 0u);
+  std::vector<int32_t> perm(slots, -1);
+  for (int row = 0; row < rows; ++row)
+    for (int lane = 0; lane < 32; ++lane) {
+      const int32_t t = slot_t[row * 32 + lane];
+      const int q = row / 8, w = row % 8;
+      const int idx = q * 256 + w * 32 + lane;
+      perm[idx] = t;
+      if (t < 0) continue;
+      const int k = K[t];
+      const uint32_t off = (uint32_t)srht::ws_phys(k & ((1 << 14) - 1)) * 4u;
+      const uint32_t kmid = (uint32_t)(k >> 14) & (uint32_t)(P->J2 - 1);
+      uint32_t rev = 0;
+      for (int i = 0; i < P->log_j2; ++i) rev |= ((kmid >> i) & 1u) << (31 - i);
+      meta[idx] = off | rev;
+    }
+  if ((e = cudaMalloc(&P->d_meta, slots * sizeof(uint32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&P->d_perm, slots * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMemcpy(P->d_meta, meta.data(), slots * sizeof(uint32_t), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+  return cudaMemcpy(P->d_perm, perm.data(), slots * sizeof(int32_t), cudaMemcpyHostToDevice);
 }
 
 srht::SketchParams base_params(const srht_plan* P) {
@@ -82,7 +135,67 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
   int dev = -1;
   if (cudaGetDevice(&dev) != cudaSuccess) return SRHT_ECUDA;
   if (dev != P->device) return SRHT_EINVAL;
-  cudaError_t e = srht::launch_sketch(P, sp, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool batched = sp.cols_per_problem != INT64_MAX;
+  if (P->ws_ok && !batched) {
+    // dense sources -> kernel v2; CSC sources -> kernel v1 (separate launches)
+    srht::ColSrc dense[2], csc[2];
+    int nd = 0, ncsc = 0;
+    const int nsrc = sp.total_cols > sp.ncols0 ? 2 : 1;
+    for (int i = 0; i < nsrc; ++i) {
+      if (sp.src[i].ncols <= 0) continue;
+      if (sp.src[i].fmt == SRHT_DENSE) dense[nd++] = sp.src[i]; else csc[ncsc++] = sp.src[i];
+    }
+    if (nd) {
+      srht::WsParams wp;
+      std::memset(&wp, 0, sizeof(wp));
+      wp.src[0] = dense[0];
+      wp.ncols0 = dense[0].ncols;
+      wp.total_cols = dense[0].ncols;
+      if (nd == 2) {
+        wp.src[1] = dense[1];
+        wp.total_cols += dense[1].ncols;
+      }
+      wp.signs = sp.signs;
+      wp.meta = P->d_meta;
+      wp.perm = P->d_perm;
+      wp.r = P->r;
+      wp.n = P->n;
+      wp.J = P->J2;
+      wp.n_sub = P->n_sub2;
+      wp.S_act = P->S_act2;
+      wp.n_items = wp.total_cols * P->S_act2;
+      wp.scale = P->scale;
+      wp.partials = sp.partials;
+      const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
+      if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
+      cudaError_t e = srht::launch_sketch_ws(P, wp, st);
+      if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot + 1], st);
+      if (e != cudaSuccess) return SRHT_ECUDA;
+      if (P->S_act2 > 1) {
+        srht::SketchParams rp = sp;
+        rp.src[0] = wp.src[0];
+        rp.src[1] = wp.src[1];
+        rp.ncols0 = wp.ncols0;
+        rp.total_cols = wp.total_cols;
+        rp.S_act = P->S_act2;
+        if (srht::launch_reduce(rp, 14 + P->log_j2, st) != cudaSuccess) return SRHT_ECUDA;
+      }
+    }
+    if (ncsc) {
+      srht::SketchParams cp = sp;
+      cp.src[0] = csc[0];
+      cp.ncols0 = csc[0].ncols;
+      cp.total_cols = csc[0].ncols;
+      if (ncsc == 2) {
+        cp.src[1] = csc[1];
+        cp.total_cols += csc[1].ncols;
+      }
+      if (srht::launch_sketch(P, cp, st) != cudaSuccess) return SRHT_ECUDA;
+    }
+    return SRHT_OK;
+  }
+  cudaError_t e = srht::launch_sketch(P, sp, st);
   return e == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
 }
 
@@ -160,8 +273,21 @@ srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t s
     srht_plan_destroy(P);
     return SRHT_ECUDA;
   }
-  const cudaError_t e = srht::build_plan_device(P, st);
+  cudaError_t e = srht::build_plan_device(P, st);
   cudaStreamDestroy(st);
+  // Kernel v2 geometry (dense single problems): B = 2^14, slabs of 2^20 rows.
+  if (e == cudaSuccess && batch == 1 && N >= (int64_t(1) << 14) && r <= 16384) {
+    P->ws_ok = true;
+    const int64_t NB2 = N >> 14;
+    int lj2 = 6;
+    while ((int64_t(1) << lj2) > NB2) --lj2;
+    P->log_j2 = lj2;
+    P->J2 = int64_t(1) << lj2;
+    P->n_sub2 = (n + (1 << 14) - 1) >> 14;
+    P->S_act2 = (P->n_sub2 + P->J2 - 1) / P->J2;
+    P->rpt2 = r <= 8 * 256 ? 8 : r <= 16 * 256 ? 16 : r <= 32 * 256 ? 32 : 64;
+    e = build_ws_layout(P);
+  }
   if (e != cudaSuccess) {
     srht_plan_destroy(P);
     return e == cudaErrorMemoryAllocation ? SRHT_ENOMEM : SRHT_ECUDA;
@@ -178,6 +304,8 @@ srht_status srht_plan_destroy(srht_plan* P) {
   if (!P) return SRHT_OK;
   cudaFree(P->d_signs);
   cudaFree(P->d_K);
+  cudaFree(P->d_meta);
+  cudaFree(P->d_perm);
   delete P;
   return SRHT_OK;
 }
@@ -254,10 +382,44 @@ srht_status srht_sketch_batched(const srht_plan* P, const srht_matrix* M, float*
   return run(P, sp, ws, ws_bytes, stream);
 }
 
-srht_status srht_profile_set_events(void* before, void* after) {
-  srht::g_prof_before = static_cast<cudaEvent_t>(before);
-  srht::g_prof_after = static_cast<cudaEvent_t>(after);
+srht_status srht_profile_start(int capacity) {
+  if (capacity < 1 || srht::g_prof.on) return SRHT_EINVAL;
+  srht::ProfileState& g = srht::g_prof;
+  g.ev = new (std::nothrow) cudaEvent_t[2 * (size_t)capacity];
+  if (!g.ev) return SRHT_ENOMEM;
+  for (int i = 0; i < 2 * capacity; ++i) {
+    if (cudaEventCreate(&g.ev[i]) != cudaSuccess) {
+      for (int k = 0; k < i; ++k) cudaEventDestroy(g.ev[k]);
+      delete[] g.ev;
+      g.ev = nullptr;
+      return SRHT_ECUDA;
+    }
+  }
+  g.capacity = capacity;
+  g.used = 0;
+  g.on = true;
   return SRHT_OK;
+}
+
+srht_status srht_profile_stop(float* ms, int capacity, int* count) {
+  srht::ProfileState& g = srht::g_prof;
+  if (!g.on) return SRHT_EINVAL;
+  srht_status st = SRHT_OK;
+  int n = 0;
+  for (int i = 0; i < g.used; ++i) {
+    float t = 0.f;
+    if (cudaEventSynchronize(g.ev[2 * i + 1]) != cudaSuccess ||
+        cudaEventElapsedTime(&t, g.ev[2 * i], g.ev[2 * i + 1]) != cudaSuccess) {
+      st = SRHT_ECUDA;
+      break;
+    }
+    if (ms && i < capacity) ms[n++] = t;
+  }
+  if (count) *count = n;
+  for (int i = 0; i < 2 * g.capacity; ++i) cudaEventDestroy(g.ev[i]);
+  delete[] g.ev;
+  g = srht::ProfileState();
+  return st;
 }
 
 srht_status srht_gen_uniform(uint64_t seed, uint64_t stream0, int64_t rows, int64_t cols, float* out, int64_t ld,

@@ -24,6 +24,13 @@ struct srht_plan {
   int device;
   uint64_t* d_signs;  // [batch][words64]
   int32_t* d_K;       // [batch][r], ascending
+  // Kernel v2 (dense, warp-specialized, B = 2^14): geometry + consumer slot layout.
+  bool ws_ok;         // single problem, N >= 2^14, r <= 16384
+  int log_j2;
+  int64_t J2, n_sub2, S_act2;
+  int rpt2;           // consumer accumulators per thread (8/16/32/64)
+  uint32_t* d_meta;   // [rpt2*256]: byte offset of phys(k_lo) | reversed k_mid << 17
+  int32_t* d_perm;    // [rpt2*256]: sample index t or -1
 };
 
 namespace srht {
@@ -65,7 +72,31 @@ struct SketchParams {
 
 cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream_t stream);
 
-extern cudaEvent_t g_prof_before, g_prof_after;  // srht_profile_set_events
+// Kernel v2 (sketch_ws.cu): dense columns only.
+struct WsParams {
+  ColSrc src[2];
+  int64_t ncols0, total_cols;
+  const uint32_t* signs;  // problem 0
+  const uint32_t* meta;
+  const int32_t* perm;
+  int64_t r, n;
+  int64_t J, n_sub, S_act;
+  int64_t n_items;        // total_cols * S_act
+  float scale;
+  float* partials;        // [S_act][total_cols][r] when S_act > 1
+};
+cudaError_t launch_sketch_ws(const srht_plan* P, const WsParams& wp, cudaStream_t stream);
+int ws_phys(int x);  // tile layout of kernel v2 (host side, for the slot layout)
+// Fixed-order slab reduction shared by both kernels.
+cudaError_t launch_reduce(const SketchParams& sp, int slab_shift, cudaStream_t stream);
+
+// Profiling (srht_profile_start/stop): event pairs around the tile kernel.
+struct ProfileState {
+  bool on = false;
+  int capacity = 0, used = 0;
+  cudaEvent_t* ev = nullptr;  // 2 * capacity
+};
+extern ProfileState g_prof;
 
 cudaError_t launch_gen_uniform(uint64_t seed, uint64_t stream0, int64_t rows, int64_t cols,
                                float* out, int64_t ld, cudaStream_t stream);

@@ -322,13 +322,14 @@ cudaError_t launch_b(int rpt, const SketchParams& sp, int64_t items, cudaStream_
 
 }  // namespace
 
-cudaEvent_t g_prof_before = nullptr, g_prof_after = nullptr;
+ProfileState g_prof;
 
 cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream_t stream) {
   if (sp.total_cols <= 0) return cudaSuccess;
   const int64_t items = sp.total_cols * sp.S_act * sp.groups;
   cudaError_t e;
-  if (g_prof_before) cudaEventRecord(g_prof_before, stream);
+  const int slot = (g_prof.on && g_prof.used < g_prof.capacity) ? g_prof.used++ : -1;
+  if (slot >= 0) cudaEventRecord(g_prof.ev[2 * slot], stream);
   switch (P->log_b) {
     case 10: e = launch_b<10>(P->rpt, sp, items, stream); break;
     case 11: e = launch_b<11>(P->rpt, sp, items, stream); break;
@@ -337,12 +338,16 @@ cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream
     case 14: e = launch_b<14>(P->rpt, sp, items, stream); break;
     default: return cudaErrorInvalidValue;
   }
-  if (g_prof_after) cudaEventRecord(g_prof_after, stream);
+  if (slot >= 0) cudaEventRecord(g_prof.ev[2 * slot + 1], stream);
   if (e != cudaSuccess || sp.S_act == 1) return e;
+  return launch_reduce(sp, P->log_b + P->log_j, stream);
+}
+
+cudaError_t launch_reduce(const SketchParams& sp, int slab_shift, cudaStream_t stream) {
   const int64_t zc = (sp.total_cols + 65534) / 65535;
   dim3 grid((unsigned)((sp.r + 255) / 256), (unsigned)(sp.total_cols < 65535 ? sp.total_cols : 65535),
             (unsigned)zc);
-  k_reduce_slabs<<<grid, 256, 0, stream>>>(sp, P->log_b + P->log_j);
+  k_reduce_slabs<<<grid, 256, 0, stream>>>(sp, slab_shift);
   return cudaGetLastError();
 }
 

@@ -49,6 +49,10 @@ def check_close(got, ref, M):
     (3 << 19, 2, 8192, 8),     # several slabs, B = 2^13
     (1 << 21, 2, 16384, 9),    # B = 2^14, two slabs
     (70000, 2, 20000, 10),     # r > 32 * threads: several sample groups
+    ((1 << 20) + 3 * 16384 + 7, 3, 8192, 11),   # v2: ragged last tile, tail slab of 4 sub-blocks
+    ((1 << 20) + 5 * 16384 + 1, 2, 16384, 12),  # v2: tail slab of 6 sub-blocks (inactive Gray steps)
+    (1 << 14, 3, 300, 13),     # v2: a single tile
+    ((1 << 14) + 1, 2, 16384, 14),  # v2: r = 16384 > n, two tiles, second holds one row
 ])
 def test_dense_random_parity(lib, n, c, r, seed):
     from oracle import srht as osr
