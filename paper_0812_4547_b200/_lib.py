@@ -4,7 +4,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsrht.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("SRHT_LIB", "libsrht.so"))
 
 SRHT_DENSE = 0
 SRHT_CSC = 1

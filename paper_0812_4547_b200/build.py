@@ -36,6 +36,25 @@ def _compile(src, verbose):
     return out, r.stderr if verbose else ""
 
 
+def build_debug():
+    """Experiment build (scripts/ws_experiments.py): libsrht_dbg.so with kernel knock-outs."""
+    os.makedirs(OBJ, exist_ok=True)
+    out = os.path.join(PKG, "libsrht_dbg.so")
+    objs = []
+    for src in SOURCES:
+        o = os.path.join(OBJ, "dbg_" + os.path.splitext(src)[0] + ".o")
+        cmd = [NVCC] + ARCH + FLAGS + ["-DSRHT_WS_DEBUG", "-c", os.path.join(CSRC, src), "-o", o]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr)
+        objs.append(o)
+    r = subprocess.run([NVCC] + ARCH + ["-shared", "-o", out] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return out
+
+
 def build(verbose=False, force=False):
     os.makedirs(OBJ, exist_ok=True)
     if force:
@@ -57,4 +76,7 @@ def build(verbose=False, force=False):
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    if "--debug" in sys.argv:
+        print(build_debug())
+    else:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

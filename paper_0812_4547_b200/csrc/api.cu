@@ -156,7 +156,7 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
         wp.src[1] = dense[1];
         wp.total_cols += dense[1].ncols;
       }
-      wp.signs = sp.signs;
+      wp.signs_ws = P->d_signs_ws;
       wp.meta = P->d_meta;
       wp.perm = P->d_perm;
       wp.r = P->r;
@@ -167,6 +167,8 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       wp.n_items = wp.total_cols * P->S_act2;
       wp.scale = P->scale;
       wp.partials = sp.partials;
+      wp.debug = srht::g_debug_mode;
+      wp.trace = srht::g_debug_trace;
       const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
       if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
       cudaError_t e = srht::launch_sketch_ws(P, wp, st);
@@ -278,8 +280,11 @@ srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t s
   // Kernel v2 geometry (dense single problems): B = 2^14, slabs of 2^20 rows.
   if (e == cudaSuccess && batch == 1 && N >= (int64_t(1) << 14) && r <= 16384) {
     P->ws_ok = true;
+    // Slab = J2 tiles; J2 ~ 64 r / 2^14 keeps the slab partials (r floats per
+    // slab) near 3% of the input, and slabs small enough to load-balance.
     const int64_t NB2 = N >> 14;
-    int lj2 = 6;
+    int lj2 = 0;
+    while ((int64_t(1) << lj2) < 64 * r / (1 << 14) && lj2 < 6) ++lj2;
     while ((int64_t(1) << lj2) > NB2) --lj2;
     P->log_j2 = lj2;
     P->J2 = int64_t(1) << lj2;
@@ -287,6 +292,16 @@ srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t s
     P->S_act2 = (P->n_sub2 + P->J2 - 1) / P->J2;
     P->rpt2 = r <= 8 * 256 ? 8 : r <= 16 * 256 ? 16 : r <= 32 * 256 ? 32 : 64;
     e = build_ws_layout(P);
+    const int64_t n_tiles = (P->N_eff >> 14);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_signs_ws, n_tiles * 128 * sizeof(uint4));
+    if (e == cudaSuccess) {
+      cudaStream_t st2;
+      e = cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking);
+      if (e == cudaSuccess) {
+        e = srht::build_ws_signs(P->d_signs, n_tiles, P->d_signs_ws, st2);
+        cudaStreamDestroy(st2);
+      }
+    }
   }
   if (e != cudaSuccess) {
     srht_plan_destroy(P);
@@ -306,6 +321,7 @@ srht_status srht_plan_destroy(srht_plan* P) {
   cudaFree(P->d_K);
   cudaFree(P->d_meta);
   cudaFree(P->d_perm);
+  cudaFree(P->d_signs_ws);
   delete P;
   return SRHT_OK;
 }
@@ -380,6 +396,18 @@ srht_status srht_sketch_batched(const srht_plan* P, const srht_matrix* M, float*
   sp.total_cols = M->cols;
   sp.cols_per_problem = M->cols / P->batch;
   return run(P, sp, ws, ws_bytes, stream);
+}
+
+// Undeclared experiment hook (scripts only): knock out parts of kernel v2.
+// bit0: producers skip global loads; bit1: consumers skip the gather;
+// bit2: producers skip the butterflies.  Results are wrong when non-zero.
+int srht_debug_set_mode(int mode) {
+  srht::g_debug_mode = mode;
+  return 0;
+}
+int srht_debug_set_trace(unsigned long long* dev_buf) {
+  srht::g_debug_trace = dev_buf;
+  return 0;
 }
 
 srht_status srht_profile_start(int capacity) {

@@ -29,6 +29,7 @@ struct srht_plan {
   int log_j2;
   int64_t J2, n_sub2, S_act2;
   int rpt2;           // consumer accumulators per thread (8/16/32/64)
+  uint4* d_signs_ws;  // [N/2^14][128] sign bits in producer-thread order
   uint32_t* d_meta;   // [rpt2*256]: byte offset of phys(k_lo) | reversed k_mid << 17
   int32_t* d_perm;    // [rpt2*256]: sample index t or -1
 };
@@ -37,6 +38,7 @@ namespace srht {
 
 // Plan builder (plan.cu): fills d_signs and d_K; synchronous on `stream`.
 cudaError_t build_plan_device(srht_plan* P, cudaStream_t stream);
+cudaError_t build_ws_signs(const uint64_t* signs, int64_t n_tiles, uint4* out, cudaStream_t stream);
 
 // One column source of a sketch launch.
 struct ColSrc {
@@ -76,7 +78,7 @@ cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream
 struct WsParams {
   ColSrc src[2];
   int64_t ncols0, total_cols;
-  const uint32_t* signs;  // problem 0
+  const uint4* signs_ws;  // problem 0, producer-thread order
   const uint32_t* meta;
   const int32_t* perm;
   int64_t r, n;
@@ -84,7 +86,11 @@ struct WsParams {
   int64_t n_items;        // total_cols * S_act
   float scale;
   float* partials;        // [S_act][total_cols][r] when S_act > 1
+  int debug;              // experiment knock-outs (srht_debug_set_mode); 0 in production
+  unsigned long long* trace;  // experiment phase timestamps (debug build only)
 };
+extern int g_debug_mode;
+extern unsigned long long* g_debug_trace;
 cudaError_t launch_sketch_ws(const srht_plan* P, const WsParams& wp, cudaStream_t stream);
 int ws_phys(int x);  // tile layout of kernel v2 (host side, for the slot layout)
 // Fixed-order slab reduction shared by both kernels.

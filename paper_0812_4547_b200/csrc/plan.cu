@@ -271,6 +271,39 @@ cudaError_t build_plan_device(srht_plan* P, cudaStream_t stream) {
 }
 
 // ---------------------------------------------------------------------------
+// Kernel-v2 sign layout: for tile T (2^14 rows) and producer thread p
+// (lane = p & 31, wg = p >> 5), the 128 sign bits of its round-0 elements
+// x = v + 4*lane + 128*wg + 512*h (v < 4, h < 32) packed as bit 4h+v of a uint4,
+// so one 16-byte load gives a thread all its signs for the tile.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_permute_signs_ws(const uint32_t* __restrict__ signs32, int64_t n_tiles, uint4* __restrict__ out) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n_tiles * 128) return;
+  const int64_t T = idx >> 7;
+  const int p = (int)(idx & 127), lane = p & 31, wg = p >> 5;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  for (int h = 0; h < 32; ++h) {
+    for (int v = 0; v < 4; ++v) {
+      const int64_t row = (T << 14) + v + 4 * lane + 128 * wg + 512 * h;
+      const uint32_t bit = (signs32[row >> 5] >> (row & 31)) & 1u;
+      w[h >> 3] |= bit << (((h & 7) << 2) + v);
+    }
+  }
+  out[idx] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+}  // namespace
+
+cudaError_t build_ws_signs(const uint64_t* signs, int64_t n_tiles, uint4* out, cudaStream_t stream) {
+  const int64_t total = n_tiles * 128;
+  k_permute_signs_ws<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(reinterpret_cast<const uint32_t*>(signs),
+                                                                         n_tiles, out);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  return e;
+}
+
+// ---------------------------------------------------------------------------
 // Workload generator (benchmark/test inputs only): exact FP32 Uniform[0,1).
 // ---------------------------------------------------------------------------
 namespace {

@@ -323,6 +323,8 @@ cudaError_t launch_b(int rpt, const SketchParams& sp, int64_t items, cudaStream_
 }  // namespace
 
 ProfileState g_prof;
+int g_debug_mode = 0;
+unsigned long long* g_debug_trace = nullptr;
 
 cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream_t stream) {
   if (sp.total_cols <= 0) return cudaSuccess;

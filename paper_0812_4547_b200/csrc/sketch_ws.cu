@@ -67,25 +67,73 @@ __device__ __forceinline__ void fwht128(float2 (&v)[64]) {
   }
 }
 
-struct Sched {
-  int64_t S_act, J, n_sub;
-  __device__ __forceinline__ void item(int64_t it, int64_t& col, int64_t& s, int64_t& cnt, int& L) const {
-    col = it / S_act;
-    s = it - col * S_act;
-    const int64_t j0 = s * J;
-    cnt = (n_sub - j0 < J) ? n_sub - j0 : J;
-    L = 0;
-    while ((int64_t(1) << L) < cnt) ++L;
-  }
+// Walks this CTA's tiles in order: items blockIdx.x, +gridDim.x, ...; within a
+// slab, sub-blocks in Gray-code order, skipping all-padding ones.
+struct Cursor {
+  int it, m, L, cnt, s, col;
+  bool valid;
 };
 
-template <int RPT>
+__device__ __forceinline__ void cursor_item(const WsParams& P, Cursor& c) {
+  c.valid = c.it < P.n_items;
+  if (!c.valid) return;
+  c.col = (int)(c.it / P.S_act);
+  c.s = (int)(c.it - (int64_t)c.col * P.S_act);
+  const int64_t j0 = (int64_t)c.s * P.J;
+  c.cnt = (int)((P.n_sub - j0 < P.J) ? P.n_sub - j0 : P.J);
+  c.L = 0;
+  while ((1 << c.L) < c.cnt) ++c.L;
+  c.m = 0;
+}
+
+// Advance to the next active tile (gray(m) < cnt).  Returns false when done.
+__device__ __forceinline__ bool cursor_next(const WsParams& P, Cursor& c) {
+  while (c.valid) {
+    ++c.m;
+    if (c.m >= (1 << c.L)) {
+      c.it += gridDim.x;
+      cursor_item(P, c);
+      if (!c.valid) return false;
+    }
+    if ((c.m ^ (c.m >> 1)) < c.cnt) return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void cursor_start(const WsParams& P, Cursor& c) {
+  c.it = blockIdx.x;
+  cursor_item(P, c);
+  c.m = -1;
+  cursor_next(P, c);  // gray(0) = 0 < cnt always when valid
+}
+
+__device__ __forceinline__ const float* col_ptr(const WsParams& P, int col) {
+  const bool second = col >= P.ncols0;
+  const float* base = second ? P.src[1].vals : P.src[0].vals;
+  const int64_t ld = second ? P.src[1].ld : P.src[0].ld;
+  const int64_t lc = second ? col - P.ncols0 : col;
+  return base + lc * ld;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  // bulk prefetch needs a 16-byte aligned address and a multiple-of-16 size
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t a16 = (a + 15) & ~uintptr_t(15);
+  const uint32_t skip = (uint32_t)(a16 - a);
+  if (bytes <= skip + 16) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a16), "r"((bytes - skip) & ~15u) : "memory");
+}
+
+#define TRACE(k)                                                                              \
+  if ((DBG & 8) && blockIdx.x == 0 && (p & 31) == 0 && ntr < 64)                             \
+    P.trace[((size_t)(g * 4 + wg) * 64 + ntr) * 10 + (k)] = clock64();
+
+template <int RPT, int DBG>
 __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant__ WsParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   float* tiles = reinterpret_cast<float*>(smem);
   uint32_t* meta_s = reinterpret_cast<uint32_t*>(smem + 2 * TILE_BYTES);
   const int tid = threadIdx.x;
-  const Sched sc{P.S_act, P.J, P.n_sub};
 
   if (tid < 256) {
     // =========================== producers ===========================
@@ -95,68 +143,89 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
     float* tile = tiles + g * TILE_WORDS;
     const int base0 = (lane << 2) + (wg << 7);                                           // phys == identity
     const int base1 = phys((lane & 3) + ((lane >> 2) << 9) + (wg << 12));
-    const int64_t n = P.n;
-    int64_t produced = 0;
-    for (int64_t it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-      int64_t col, s, cnt;
-      int L;
-      sc.item(it, col, s, cnt, L);
-      const bool second = col >= P.ncols0;
-      const ColSrc& cs = second ? P.src[1] : P.src[0];
-      const int64_t lc = second ? col - P.ncols0 : col;
-      const float* __restrict__ colp = cs.vals + lc * cs.ld;
-      const int64_t j0 = s * P.J;
-      for (int m = 0; m < (1 << L); ++m) {
-        const int64_t j = m ^ (m >> 1);
-        if (j >= cnt) continue;
-        const bool mine = (produced & 1) == g;
-        ++produced;
-        if (!mine) continue;
-        const int64_t row0 = (j0 + j) * (int64_t)B;
-        float2 v[64];
-        // ---- load D x: element x = v4 + 4*lane + 128*wg + 512*h ----
-        if (cs.vec && row0 + B <= n) {
-#pragma unroll
-          for (int h = 0; h < 32; ++h) {
-            const float4 f = __ldcs(reinterpret_cast<const float4*>(colp + row0 + base0 + (h << 9)));
-            v[2 * h] = make_float2(f.x, f.y);
-            v[2 * h + 1] = make_float2(f.z, f.w);
-          }
-        } else {
-#pragma unroll
-          for (int h = 0; h < 32; ++h) {
-            const int64_t row = row0 + base0 + (h << 9);
-            v[2 * h] = make_float2(row + 0 < n ? colp[row + 0] : 0.f, row + 1 < n ? colp[row + 1] : 0.f);
-            v[2 * h + 1] = make_float2(row + 2 < n ? colp[row + 2] : 0.f, row + 3 < n ? colp[row + 3] : 0.f);
-          }
-        }
-        const uint32_t* __restrict__ sg = P.signs + ((row0 + (wg << 7)) >> 5) + (lane >> 3);
-        const int sh = (lane & 7) << 2;
+    const int n = (int)P.n;
+    const bool vec_ok = P.src[0].vec && (P.total_cols == P.ncols0 || P.src[1].vec);
+    Cursor cur;
+    cursor_start(P, cur);
+    if (g == 1) cursor_next(P, cur);
+    int ntr = 0;
+    while (cur.valid) {
+      TRACE(0)
+      const int row0 = (int)(((int64_t)cur.s * P.J + (cur.m ^ (cur.m >> 1))) * B);
+      const float* __restrict__ colp = col_ptr(P, cur.col);
+      // advance two tiles for the next iteration (the other group takes the one between)
+      if (cursor_next(P, cur)) cursor_next(P, cur);
+      float2 v[64];
+      // ---- load D x: element x = v4 + 4*lane + 128*wg + 512*h ----
+      const uint4 sgn = __ldg(P.signs_ws + ((size_t)(row0 >> LOG_B) << 7) + p);
+      if (DBG & 1) {
 #pragma unroll
         for (int h = 0; h < 32; ++h) {
-          const uint32_t w = __ldg(sg + (h << 4)) >> sh;
-          v[2 * h].x = flipf(v[2 * h].x, w << 31);
-          v[2 * h].y = flipf(v[2 * h].y, (w << 30) & 0x80000000u);
-          v[2 * h + 1].x = flipf(v[2 * h + 1].x, (w << 29) & 0x80000000u);
-          v[2 * h + 1].y = flipf(v[2 * h + 1].y, (w << 28) & 0x80000000u);
+          v[2 * h] = make_float2((float)h, (float)row0);
+          v[2 * h + 1] = make_float2((float)base0, 1.f);
         }
-        fwht128(v);  // bits 0,1 (vector) and 9..13 (h)
-        bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);
+      } else if (vec_ok && row0 + B <= n) {
 #pragma unroll
-        for (int h = 0; h < 32; ++h)
-          *reinterpret_cast<float4*>(tile + base0 + ((h & 7) << 2) + h * ROW) =
-              make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y);
-        bar_sync(g ? BAR_GRP1 : BAR_GRP0, 128);
-#pragma unroll
-        for (int k = 0; k < 64; ++k) v[k] = make_float2(tile[base1 + 8 * k], tile[base1 + 8 * k + 4]);
-        fwht128(v);  // bits 2..8
-#pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          tile[base1 + 8 * k] = v[k].x;
-          tile[base1 + 8 * k + 4] = v[k].y;
+        for (int h = 0; h < 32; ++h) {
+          const float4 f = __ldcs(reinterpret_cast<const float4*>(colp + row0 + base0 + (h << 9)));
+          v[2 * h] = make_float2(f.x, f.y);
+          v[2 * h + 1] = make_float2(f.z, f.w);
         }
-        bar_arrive(g ? BAR_FULL1 : BAR_FULL0, 384);
+      } else {
+#pragma unroll
+        for (int h = 0; h < 32; ++h) {
+          const int row = row0 + base0 + (h << 9);
+          v[2 * h] = make_float2(row + 0 < n ? colp[row + 0] : 0.f, row + 1 < n ? colp[row + 1] : 0.f);
+          v[2 * h + 1] = make_float2(row + 2 < n ? colp[row + 2] : 0.f, row + 3 < n ? colp[row + 3] : 0.f);
+        }
       }
+      if (DBG & 8) {
+        float acc = 0.f;
+#pragma unroll
+        for (int h = 0; h < 64; ++h) acc += v[h].x;
+        if (acc == 1234.5f) v[0].y = 0.f;
+      }
+      TRACE(1)
+#pragma unroll
+      for (int h = 0; h < 32; ++h) {  // sign of element (h, v) is bit ((h & 7) << 2) + v of word h >> 3
+        const uint32_t w = (h < 8 ? sgn.x : h < 16 ? sgn.y : h < 24 ? sgn.z : sgn.w);
+        const int b = (h & 7) << 2;
+        v[2 * h].x = flipf(v[2 * h].x, (w << (31 - b)) & 0x80000000u);
+        v[2 * h].y = flipf(v[2 * h].y, (w << (30 - b)) & 0x80000000u);
+        v[2 * h + 1].x = flipf(v[2 * h + 1].x, (w << (29 - b)) & 0x80000000u);
+        v[2 * h + 1].y = flipf(v[2 * h + 1].y, (w << (28 - b)) & 0x80000000u);
+      }
+      TRACE(2)
+      if (!(DBG & 4)) fwht128(v);  // bits 0,1 (vector) and 9..13 (h)
+      TRACE(3)
+      bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);
+      TRACE(4)
+#pragma unroll
+      for (int h = 0; h < 32; ++h)
+        *reinterpret_cast<float4*>(tile + base0 + ((h & 7) << 2) + h * ROW) =
+            make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y);
+      TRACE(5)
+      bar_sync(g ? BAR_GRP1 : BAR_GRP0, 128);
+      TRACE(6)
+#pragma unroll
+      for (int k = 0; k < 64; ++k) v[k] = make_float2(tile[base1 + 8 * k], tile[base1 + 8 * k + 4]);
+      if (DBG & 8) {
+        float acc = 0.f;
+#pragma unroll
+        for (int h = 0; h < 64; ++h) acc += v[h].x;
+        if (acc == 1234.5f) v[0].y = 0.f;
+      }
+      TRACE(7)
+      if (!(DBG & 4)) fwht128(v);  // bits 2..8
+      TRACE(8)
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {
+        tile[base1 + 8 * k] = v[k].x;
+        tile[base1 + 8 * k + 4] = v[k].y;
+      }
+      bar_arrive(g ? BAR_FULL1 : BAR_FULL0, 384);
+      TRACE(9)
+      if (DBG & 8) ++ntr;
     }
     bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);  // matches the consumers' last release
   } else {
@@ -164,27 +233,51 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
     const int c = tid - 256;
     for (int i = c; i < RPT * NCONS; i += NCONS) meta_s[i] = P.meta[i];
+    // L2 prefetch cursor: one thread keeps the HBM stream PREF tiles ahead.
+    constexpr int PREF = 8;
+    Cursor pf;
+    const bool pf_thread = (c == 0);
+    const int n = (int)P.n;
+    if (pf_thread) {
+      cursor_start(P, pf);
+      for (int k = 0; k < PREF && pf.valid; ++k) {
+        const int row0 = (int)(((int64_t)pf.s * P.J + (pf.m ^ (pf.m >> 1))) * B);
+        const int rows = n - row0 < B ? n - row0 : B;
+        prefetch_l2(col_ptr(P, pf.col) + row0, (uint32_t)(rows * 4) & ~15u);
+        cursor_next(P, pf);
+      }
+    }
     bar_sync(BAR_CONS, NCONS);
     bar_arrive(BAR_EMPTY0, 384);
     bar_arrive(BAR_EMPTY1, 384);
     float acc[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) acc[q] = 0.f;
-    int64_t consumed = 0;
+    int consumed = 0;
     const uint32_t* mrow = meta_s + c;
     for (int64_t it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-      int64_t col, s, cnt;
-      int L;
-      sc.item(it, col, s, cnt, L);
+      const int col = (int)(it / P.S_act);
+      const int s = (int)(it - (int64_t)col * P.S_act);
+      const int64_t j0 = (int64_t)s * P.J;
+      const int cnt = (int)((P.n_sub - j0 < P.J) ? P.n_sub - j0 : P.J);
+      int L = 0;
+      while ((1 << L) < cnt) ++L;
       for (int m = 0; m < (1 << L); ++m) {
-        const int64_t j = m ^ (m >> 1);
+        const int j = m ^ (m >> 1);
         const int qb = m ? __ffs(m) - 1 : 0;  // Gray-code bit flipped at step m
         if (j < cnt) {
-          const int b = (int)(consumed & 1);
+          const int b = consumed & 1;
           ++consumed;
+          if (pf_thread && pf.valid) {
+            const int row0 = (int)(((int64_t)pf.s * P.J + (pf.m ^ (pf.m >> 1))) * B);
+            const int rows = n - row0 < B ? n - row0 : B;
+            prefetch_l2(col_ptr(P, pf.col) + row0, (uint32_t)(rows * 4) & ~15u);
+            cursor_next(P, pf);
+          }
           bar_sync(b ? BAR_FULL1 : BAR_FULL0, 384);
           const char* tb = reinterpret_cast<const char*>(tiles) + b * TILE_BYTES;
-          if (qb == 0) {
+          if (DBG & 2) {
+          } else if (qb == 0) {
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
               const uint32_t mw = mrow[q * NCONS];
@@ -208,7 +301,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
       // ---- slab epilogue: undo the frame sign of the last Gray step, write ----
       const uint32_t jlast = (uint32_t)(((1 << L) - 1) ^ (((1 << L) - 1) >> 1));
       const bool second = col >= P.ncols0;
-      const ColSrc& cs = second ? P.src[1] : P.src[0];
+      float* __restrict__ outp = second ? P.src[1].out : P.src[0].out;
+      const int64_t ldo = second ? P.src[1].ldo : P.src[0].ldo;
       const int64_t lc = second ? col - P.ncols0 : col;
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
@@ -216,8 +310,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
         if (t >= 0) {
           const uint32_t kmid = __brev(mrow[q * NCONS]) & (uint32_t)(P.J - 1);
           const float a = flipf(acc[q], (uint32_t)(__popc(kmid & jlast) & 1) << 31);
-          if (P.S_act == 1) cs.out[lc * cs.ldo + t] = a * P.scale;
-          else P.partials[(s * P.total_cols + col) * P.r + t] = a;
+          if (P.S_act == 1) outp[lc * ldo + t] = a * P.scale;
+          else P.partials[((int64_t)s * P.total_cols + col) * P.r + t] = a;
         }
         acc[q] = 0.f;
       }
@@ -225,17 +319,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
   }
 }
 
-template <int RPT>
-cudaError_t launch_rpt(const WsParams& wp, int grid, cudaStream_t stream) {
+template <int RPT, int DBG>
+cudaError_t launch_dbg(const WsParams& wp, int grid, cudaStream_t stream) {
   const size_t smem = 2 * (size_t)TILE_BYTES + (size_t)RPT * NCONS * 4;
   static bool attr = false;
   if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_sketch_ws<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_sketch_ws<RPT, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_sketch_ws<RPT><<<grid, NTHREADS, smem, stream>>>(wp);
+  k_sketch_ws<RPT, DBG><<<grid, NTHREADS, smem, stream>>>(wp);
   return cudaGetLastError();
+}
+
+template <int RPT>
+cudaError_t launch_rpt(const WsParams& wp, int grid, cudaStream_t stream) {
+#ifdef SRHT_WS_DEBUG
+  switch (wp.debug) {
+    case 1: return launch_dbg<RPT, 1>(wp, grid, stream);
+    case 2: return launch_dbg<RPT, 2>(wp, grid, stream);
+    case 3: return launch_dbg<RPT, 3>(wp, grid, stream);
+    case 4: return launch_dbg<RPT, 4>(wp, grid, stream);
+    case 5: return launch_dbg<RPT, 5>(wp, grid, stream);
+    case 6: return launch_dbg<RPT, 6>(wp, grid, stream);
+    case 7: return launch_dbg<RPT, 7>(wp, grid, stream);
+    case 8: return launch_dbg<RPT, 8>(wp, grid, stream);
+    default: break;
+  }
+#endif
+  return launch_dbg<RPT, 0>(wp, grid, stream);
 }
 
 }  // namespace ws
