@@ -266,16 +266,20 @@ def main():
     Ml = build_dense_shard(cfg, c0, c1, seed, device, srht)
     plan = srht.Plan(n, d, r, seed)
     ws = plan.workspace(cl)
-    cmax = (c + world - 1) // world
-    local_out = torch.zeros((cmax, r), dtype=torch.float32, device=device)  # row-major [col][t] = col-major r x c
-    gathered = torch.empty((world * cmax, r), dtype=torch.float32, device=device) if world > 1 else None
     stream = torch.cuda.current_stream(device)
     lib = _lib.load()
+    if world > 1:
+        from paper_0812_4547_b200 import dist as sdist
+        sdist.check_same_plan(plan, device=device)  # untimed: every rank derived the same D and S
+        full_out = torch.empty((c, r), dtype=torch.float32, device=device).t()
+    else:
+        full_out = torch.empty((c, r), dtype=torch.float32, device=device).t()
 
     def step():
-        plan.sketch_columns(Ml, out=local_out[:cl].t(), workspace=ws)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, local_out)
+            sdist.sketch_sharded(plan, Ml, c, out=full_out, workspace=ws)
+        else:
+            plan.sketch_columns(Ml, out=full_out, workspace=ws)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -310,7 +314,7 @@ def main():
     alg_bytes_launch = 4.0 * n * cl + 4.0 * r * cl  # read the shard once, write r x c_l
     achieved = alg_bytes_launch / (kms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(args.config), "kernel": "k_sketch_tiles",
+                "traffic": load_traffic(args.config), "kernel": "k_sketch_ws" if plan.N >= 16384 and r <= 16384 else "k_sketch_tiles",
                 "peak_source": "%s (MEASURED_PEAKS.json hbm_gbs)" % peak_kind if peak_kind == "measured"
                 else "fallback 6650 GB/s (B200_PROFILING.md)",
                 "kernel_ms": kms, "share_of_step": kms / ms}

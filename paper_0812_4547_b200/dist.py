@@ -1,0 +1,102 @@
+"""Column-sharded SRHT across ranks (one process per GPU, torch.distributed).
+
+Columns of M = [A | b] are independent given the plan, and every rank derives
+the same D and kept rows from the same seed (R4-R6), so rank k sketches
+a contiguous column range with no communication and one all-gather assembles
+the r x c result (one plan for every column).  The gathered
+buffer is column-major r x c as soon as shards are equal-sized; uneven shards
+are padded to ceil(c / world) columns for ``all_gather_into_tensor`` and
+compacted afterwards.  With the NCCL backend the gather runs over NVLink /
+NVSwitch; the tile and slab geometry depend only on (n, r), so the result is
+bit-identical to a single-GPU sketch.
+"""
+
+import hashlib
+
+import torch
+import torch.distributed as dist
+
+
+def column_range(c, world, rank):
+    """Contiguous shard [c0, c1) of c columns for `rank` (first c % world ranks get one more)."""
+    base, rem = divmod(int(c), int(world))
+    c0 = rank * base + min(rank, rem)
+    return c0, c0 + base + (1 if rank < rem else 0)
+
+
+def plan_digest(plan):
+    """64-bit digest of a plan (N, r, seed, kept rows, sign words) for cross-rank checks."""
+    h = hashlib.blake2b(digest_size=8)
+    h.update(("%d,%d,%d" % (plan.N, plan.r, plan.seed)).encode())
+    h.update(plan.indices().tobytes())
+    h.update(plan.sign_words().tobytes())
+    return int.from_bytes(h.digest(), "little") & ((1 << 63) - 1)
+
+
+def check_same_plan(plan, group=None, device=None):
+    """Raise if the ranks in `group` do not hold the same plan."""
+    d = torch.tensor([plan_digest(plan)], dtype=torch.int64, device=device)
+    world = dist.get_world_size(group)
+    out = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out, d, group=group)
+    if not bool(torch.all(out == out[0])):
+        raise RuntimeError("ranks hold different SRHT plans: %s" % out.tolist())
+
+
+def sketch_sharded(plan, M_shard, total_cols, group=None, out=None, sketch_fn=None, workspace=None):
+    """Sketch this rank's column shard and all-gather the full r x total_cols result.
+
+    plan:       srht Plan (same seed on every rank)
+    M_shard:    this rank's columns [c0, c1) of M (column_range), column-major
+    total_cols: c, the number of columns over all ranks
+    sketch_fn:  optional replacement for ``plan.sketch_columns`` with the same
+                contract (used by the CPU/gloo tests to plug in the oracle)
+    Returns a column-major (r, total_cols) tensor on M_shard's device.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    r = plan.r
+    c0, c1 = column_range(total_cols, world, rank)
+    cl = c1 - c0
+    if M_shard.shape[1] != cl:
+        raise ValueError("rank %d expects %d columns, got %d" % (rank, cl, M_shard.shape[1]))
+    cmax = -(-int(total_cols) // world)
+    dev = M_shard.device
+    # Buffers are cached on the plan so repeated calls launch nothing but the
+    # sketch kernels and the collective.  Padding rows of `local` (uneven
+    # shards) are never read back.
+    key = (world, cmax, str(dev))
+    cache = getattr(plan, "_dist_bufs", None)
+    if cache is None or cache[0] != key:
+        local_buf = torch.empty((cmax, r), dtype=torch.float32, device=dev)  # [col][t] == column-major r x cmax
+        gath_buf = torch.empty((world * cmax, r), dtype=torch.float32, device=dev)
+        try:
+            plan._dist_bufs = (key, local_buf, gath_buf)
+        except AttributeError:
+            pass
+    else:
+        _, local_buf, gath_buf = cache
+    local = local_buf
+    if cl:
+        if sketch_fn is None:
+            plan.sketch_columns(M_shard, out=local[:cl].t(), workspace=workspace)
+        else:
+            local[:cl] = sketch_fn(M_shard).t()
+    direct = (out is not None and total_cols % world == 0 and out.stride(0) == 1
+              and out.stride(1) == r and out.device == dev)
+    gathered = out.t() if direct else gath_buf
+    dist.all_gather_into_tensor(gathered, local, group=group)
+    if direct:
+        return out
+    if total_cols % world == 0:
+        full = gathered
+    else:
+        idx = []
+        for k in range(world):
+            a, b = column_range(total_cols, world, k)
+            idx.extend(range(k * cmax, k * cmax + (b - a)))
+        full = gathered.index_select(0, torch.tensor(idx, device=dev))
+    if out is not None:
+        out.copy_(full.t())
+        return out
+    return full.t()

@@ -1,0 +1,112 @@
+"""Multi-rank column sharding on CPU (gloo, world_size 2) with the oracle as the per-rank sketch.
+
+Checks the sharding / all-gather glue of paper_0812_4547_b200.dist without GPUs:
+the gathered result must equal the single-process oracle sketch exactly, for
+even and uneven shards, and mismatched plans must be detected.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_0812_4547_b200.dist import column_range, sketch_sharded
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OraclePlan:
+    """Stands in for srht.Plan on CPU: same contract, oracle arithmetic."""
+
+    def __init__(self, n, r, seed):
+        from oracle import srht as osr
+        self.n, self.r, self.seed, self.N = n, r, seed, osr.padded_size(n)
+
+    def sketch(self, M):
+        from oracle import srht as osr
+        return torch.from_numpy(osr.sketch(M.numpy().astype(np.float64), self.seed, self.r).astype(np.float32))
+
+
+def _worker(rank, world, port, n, c, r, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(123)
+        M = rng.standard_normal((n, c)).astype(np.float32)
+        c0, c1 = column_range(c, world, rank)
+        plan = OraclePlan(n, r, seed)
+        shard = torch.from_numpy(np.asfortranarray(M[:, c0:c1]))
+        full = sketch_sharded(plan, shard, c, sketch_fn=plan.sketch)
+        q.put((rank, full.contiguous().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("c", [6, 5, 1])
+def test_gloo_two_ranks_match_single_process(c):
+    n, r, seed, world = 300, 40, 7, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(k, world, port, n, c, r, seed, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle import srht as osr
+    rng = np.random.default_rng(123)
+    M = rng.standard_normal((n, c)).astype(np.float32)
+    ref = osr.sketch(M.astype(np.float64), seed, r).astype(np.float32)
+    for k in range(world):
+        assert res[k].shape == (r, c)
+        assert np.array_equal(res[k], ref)
+
+
+def test_column_range_partition():
+    for c in [1, 5, 128, 513]:
+        for world in [1, 2, 3, 4, 8]:
+            ranges = [column_range(c, world, k) for k in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == c
+            for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
+                assert a1 == b0
+            sizes = [b - a for a, b in ranges]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _digest_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        d = torch.tensor([1000 + (rank if rank == 1 else 0)], dtype=torch.int64)
+        out = torch.empty(world, dtype=torch.int64)
+        dist.all_gather_into_tensor(out, d)
+        q.put(bool(torch.all(out == out[0])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_digest_mismatch_detectable():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_digest_worker, args=(k, 2, port, q)) for k in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [False, False]
