@@ -1,0 +1,134 @@
+"""BASELINE.json configs at full size, in the launch configuration bench.py times.
+
+Element-wise parity against the oracle on sampled outputs (whole columns or
+problems the oracle can compute), the north_star tolerance
+|gpu - oracle| <= 1e-5 sqrt(n) max|col| (reading R11), and the end-to-end gate
+(reading R14): Lawson-Hanson on the GPU sketch vs on the oracle sketch, compared
+through R(x~) = ||A x~ - b|| on the original data, within 1e-6 relative.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import torch
+    import paper_0812_4547_b200 as m
+    torch.cuda.init()
+    return m
+
+
+def to_dev(M):
+    import torch
+    return torch.from_numpy(np.asfortranarray(M, dtype=np.float32)).t().contiguous().t().cuda()
+
+
+def csc_dev(lib, colptr, rowidx, vals, shape):
+    import torch
+    return lib.CSC(torch.from_numpy(np.asarray(colptr, dtype=np.int64)).cuda(),
+                   torch.from_numpy(np.asarray(rowidx, dtype=np.int32)).cuda(),
+                   torch.from_numpy(np.asarray(vals, dtype=np.float32)).cuda(), shape)
+
+
+def assert_tol(got, ref, M32):
+    bound = 1e-5 * math.sqrt(M32.shape[0]) * np.max(np.abs(M32.astype(np.float64)), axis=0)
+    err = np.abs(np.asarray(got, np.float64) - ref)
+    assert np.all(err <= bound[None, :]), float((err / np.maximum(bound, 1e-300)).max())
+    return float((err / np.maximum(bound, 1e-300)).max())
+
+
+def e2e_gate(A, b, SA_gpu, Sb_gpu, SA_ref, Sb_ref, tol=1e-6):
+    from oracle import nnls
+    x_g = nnls.solve_sketched(np.asarray(SA_gpu, np.float64), np.asarray(Sb_gpu, np.float64))
+    x_o = nnls.solve_sketched(SA_ref, Sb_ref)
+    Rg, Ro = nnls.residual_norm(A, x_g, b), nnls.residual_norm(A, x_o, b)
+    rel = abs(Rg - Ro) / Ro
+    assert rel <= tol, (rel, Rg, Ro)
+    return rel
+
+
+def test_config1_full(lib):
+    from oracle import srht as osr
+    c = workloads.CONFIGS[1]
+    n, d, r = c["n"], c["d"], c["r"]
+    M, _ = workloads.dense_host(n, d, seed=workloads.SEED)
+    plan = lib.Plan(n, d, r, workloads.SEED)
+    Md = to_dev(M)
+    SA, Sb = plan.sketch(Md[:, :d], Md[:, d])
+    got = np.column_stack([SA.cpu().numpy(), Sb.cpu().numpy()])
+    ref = osr.sketch(M.astype(np.float64), workloads.SEED, r)
+    assert_tol(got, ref, M)
+    e2e_gate(M[:, :d].astype(np.float64), M[:, d].astype(np.float64), got[:, :d], got[:, d], ref[:, :d], ref[:, d])
+
+
+def test_config2_full_batched(lib):
+    from oracle import srht as osr
+    w = workloads.config2_host(workloads.SEED)
+    n, d, batch, r = w["n"], w["d"], w["batch"], w["r"]
+    c = d + 1
+    plan = lib.Plan(n, d, r, workloads.SEED, batch=batch)
+    out = plan.sketch_batched(csc_dev(lib, w["colptr"], w["rowidx"], w["vals"], (n, batch * c))).cpu().numpy()
+    for p in list(range(0, batch, 150)) + [batch - 1]:
+        lo, hi = w["colptr"][p * c], w["colptr"][(p + 1) * c]
+        cp = w["colptr"][p * c:(p + 1) * c + 1] - lo
+        blk = workloads.csc_to_dense(cp, w["rowidx"][lo:hi], w["vals"][lo:hi], n, c)
+        ref = osr.sketch(blk, workloads.SEED, r, p=p)
+        got = out[p].T
+        assert_tol(got, ref, blk.astype(np.float32))
+        if p % 600 == 0:
+            e2e_gate(blk[:, :d], blk[:, d], got[:, :d], got[:, d], ref[:, :d], ref[:, d])
+
+
+def test_config3_full(lib):
+    import torch
+    from oracle import srht as osr
+    w = workloads.config3_host(workloads.SEED)
+    n, d, r = w["n"], w["d"], w["r"]
+    plan = lib.Plan(n, d, r, workloads.SEED)
+    SA, Sb = plan.sketch(csc_dev(lib, w["colptr"], w["rowidx"], w["vals"], (n, d)), torch.from_numpy(w["b"]).cuda())
+    got = np.column_stack([SA.cpu().numpy(), Sb.cpu().numpy()])
+    A = workloads.csc_to_dense(w["colptr"], w["rowidx"], w["vals"], n, d)
+    M = np.column_stack([A, w["b"].astype(np.float64)])
+    ref = osr.sketch(M, workloads.SEED, r)
+    assert_tol(got, ref, M.astype(np.float32))
+    e2e_gate(A, M[:, d], got[:, :d], got[:, d], ref[:, :d], ref[:, d])
+
+
+def test_config4_full_sampled_columns(lib):
+    from oracle import srht as osr
+    c = workloads.CONFIGS[4]
+    n, d, r = c["n"], c["d"], c["r"]
+    M, _ = workloads.dense_device(n, d, seed=workloads.SEED)
+    plan = lib.Plan(n, d, r, workloads.SEED)
+    SM = plan.sketch_columns(M, workspace=plan.workspace(d + 1)).cpu().numpy()
+    cols = [0, 1, 137, 255, 511, d]  # includes b
+    Mh = M[:, cols].cpu().numpy()
+    # the dense A columns are regenerated on the host bit for bit (generator pin)
+    assert np.array_equal(Mh[:, 0], workloads.host_uniform_column(workloads.SEED, 0, n))
+    ref = osr.sketch(Mh.astype(np.float64), workloads.SEED, r)
+    assert_tol(SM[:, cols], ref, Mh)
+
+
+def test_config5_full_sampled_columns(lib):
+    import torch
+    from oracle import srht as osr
+    c = workloads.CONFIGS[5]
+    n, d, r = c["n"], c["d"], c["r"]
+    M, _ = workloads.dense_device(n, d, seed=workloads.SEED)
+    plan = lib.Plan(n, d, r, workloads.SEED)
+    SM = plan.sketch_columns(M, workspace=plan.workspace(d + 1))
+    torch.cuda.synchronize()
+    SMh = SM.cpu().numpy()
+    for j in [0, 77, d]:  # two A columns and b
+        col = M[:, j].cpu().numpy()
+        ref = osr.sketch(col.astype(np.float64), workloads.SEED, r)
+        assert_tol(SMh[:, j:j + 1], ref, col[:, None])
+    del M
+    torch.cuda.empty_cache()
