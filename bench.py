@@ -258,7 +258,7 @@ def main():
         dist.init_process_group("nccl", device_id=device)
     cfg = workloads.CONFIGS[args.config]
     if cfg["kind"] != "dense":
-        raise SystemExit("bench.py measures the dense configs (1, 4, 5); sparse configs are covered by tests")
+        return bench_sparse(args, cfg, srht, _lib, world, rank, device)
     n, d, r, seed = cfg["n"], cfg["d"], cfg["r"], workloads.SEED
     c = d + 1
     c0, c1 = column_range(c, world, rank)
@@ -349,6 +349,96 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_sparse(args, cfg, srht, _lib, world, rank, device):
+    """Configs 2 (3000 batched CSC problems) and 3 (CSC A + dense b), single GPU.
+
+    Metric: input GB/s of the CSC bytes (8 nnz + 8 (c+1), plus the dense b) per
+    sketch.  These paths are FP32-ALU / latency bound (the inputs are small and
+    the transform is dense work), so the roofline reported is the FP32 add rate
+    (148 SMs x 128 lanes x SM clock) against the pruned adds per element.
+    """
+    import torch
+    if world > 1:
+        raise SystemExit("sparse configs are single-GPU in bench.py")
+    seed = workloads.SEED
+    if args.config == 2:
+        w = workloads.config2_host(seed)
+        n, d, batch, r = w["n"], w["d"], w["batch"], w["r"]
+        c = d + 1
+        ncols = batch * c
+        M = srht.CSC(torch.from_numpy(w["colptr"]).cuda(), torch.from_numpy(w["rowidx"]).cuda(),
+                     torch.from_numpy(w["vals"]).cuda(), (n, ncols))
+        plan = srht.Plan(n, d, r, seed, batch=batch)
+        out = torch.empty((batch, c, r), dtype=torch.float32, device=device)
+        ws = plan.workspace(ncols)
+
+        def step():
+            plan.sketch_batched(M, out=out, workspace=ws)
+        in_bytes = workloads.input_bytes_csc(int(w["colptr"][-1]), ncols)
+        out_bytes = 4.0 * r * ncols
+    else:
+        w = workloads.config3_host(seed)
+        n, d, r = w["n"], w["d"], w["r"]
+        ncols = d + 1
+        A = srht.CSC(torch.from_numpy(w["colptr"]).cuda(), torch.from_numpy(w["rowidx"]).cuda(),
+                     torch.from_numpy(w["vals"]).cuda(), (n, d))
+        bvec = torch.from_numpy(w["b"]).cuda()
+        plan = srht.Plan(n, d, r, seed)
+        SA = torch.empty((d, r), dtype=torch.float32, device=device).t()
+        Sb = torch.empty(r, dtype=torch.float32, device=device)
+        ws = plan.workspace(ncols)
+
+        def step():
+            plan.sketch(A, bvec, SA=SA, Sb=Sb, workspace=ws)
+        in_bytes = workloads.input_bytes_csc(int(w["colptr"][-1]), d, dense_b_rows=n)
+        out_bytes = 4.0 * r * ncols
+    # L2 flush buffer (inputs of config 3 fit in L2): 2x L2
+    flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=device)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    lib = _lib.load()
+    times = []
+    with ClockSampler(0) as clk:
+        _lib.check(lib.srht_profile_start(args.steps), "srht_profile_start")
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+        kms_arr = (ctypes.c_float * args.steps)()
+        kcount = ctypes.c_int()
+        _lib.check(lib.srht_profile_stop(kms_arr, args.steps, ctypes.byref(kcount)), "srht_profile_stop")
+    ms = statistics.mean(a.elapsed_time(b) for a, b in times)
+    kms = statistics.mean(kms_arr[i] for i in range(kcount.value)) if kcount.value else ms
+    N = plan.N
+    lb = max(10, min(14, (r - 1).bit_length()))
+    adds_per_el = lb + r / float(1 << lb)  # in-tile stages + pruned accumulate
+    adds = adds_per_el * max(N, 1 << lb) * ncols
+    clk_mhz = clk.summary()["sm_mhz"] or 1965.0
+    alu_peak = 148 * 128 * clk_mhz * 1e6 / 1e12  # T adds/s
+    value = in_bytes / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "config%d_%s" % (args.config, cfg["name"]), "n": n, "d": d, "r": r,
+                   "columns": ncols, "input_bytes": in_bytes, "output_bytes": out_bytes,
+                   "l2": "flushed (256 MB write) before each step"},
+        "roofline": {"bound": "alu", "achieved": adds / (kms * 1e-3) / 1e12, "peak": alu_peak, "unit": "Tadd/s",
+                     "frac": adds / (kms * 1e-3) / 1e12 / alu_peak, "traffic": None, "kernel": "k_sketch_tiles",
+                     "kernel_ms": kms, "adds_per_padded_element": adds_per_el,
+                     "hbm_equiv_GBps": (in_bytes + out_bytes) / (kms * 1e-3) / 1e9},
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps * (2 if plan.workspace_bytes(1) > 0 else 1),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def plan_has_reduce(plan):

@@ -74,16 +74,18 @@ cudaError_t build_ws_layout(srht_plan* P) {
     const int lo = K[t] & ((1 << 14) - 1);
     bucket[srht::ws_phys(lo) & 31].push_back((int32_t)t);
   }
+  // Deal the samples, sorted by bank, round-robin over the rows: sample i of the
+  // bank-sorted order goes to row i mod rows.  A bank with c samples then lands
+  // in min(c, rows) distinct rows, so a row holds at most ceil(max_c / rows)
+  // samples of one bank (1 when every bank has <= rows samples, 2 otherwise).
   std::vector<int32_t> slot_t(slots, -1);
-  std::vector<size_t> head(32, 0);
-  for (int row = 0; row < rows; ++row)
-    for (int b = 0; b < 32; ++b)
-      if (head[b] < bucket[b].size()) slot_t[row * 32 + b] = bucket[b][head[b]++];
-  int free_pos = 0;
+  std::vector<int> fill(rows, 0);
+  int64_t i = 0;
   for (int b = 0; b < 32; ++b)
-    while (head[b] < bucket[b].size()) {
-      while (slot_t[free_pos] >= 0) ++free_pos;
-      slot_t[free_pos] = bucket[b][head[b]++];
+    for (int32_t t : bucket[b]) {
+      const int row = (int)(i % rows);
+      slot_t[row * 32 + fill[row]++] = t;
+      ++i;
     }
   // row = q*8 + w, lane = bank  ->  meta index q*256 + 32*w + lane
   std::vector<uint32_t> meta(slots, 0u);
@@ -145,6 +147,10 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
     for (int i = 0; i < nsrc; ++i) {
       if (sp.src[i].ncols <= 0) continue;
       if (sp.src[i].fmt == SRHT_DENSE) dense[nd++] = sp.src[i]; else csc[ncsc++] = sp.src[i];
+    }
+    if (ncsc) {  // any CSC source: one kernel-v1 launch for every column (e.g. CSC A + dense b)
+      cudaError_t e = srht::launch_sketch(P, sp, st);
+      return e == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
     }
     if (nd) {
       srht::WsParams wp;
@@ -396,6 +402,17 @@ srht_status srht_sketch_batched(const srht_plan* P, const srht_matrix* M, float*
   sp.total_cols = M->cols;
   sp.cols_per_problem = M->cols / P->batch;
   return run(P, sp, ws, ws_bytes, stream);
+}
+
+// Undeclared test hook: copy the kernel-v2 consumer slot layout to the host.
+int srht_debug_copy_ws_layout(const srht_plan* P, uint32_t* meta, int32_t* perm, int* rpt2) {
+  if (!P || !P->ws_ok) return 1;
+  *rpt2 = P->rpt2;
+  if (meta && cudaMemcpy(meta, P->d_meta, P->rpt2 * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 3;
+  if (perm && cudaMemcpy(perm, P->d_perm, P->rpt2 * 256 * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 3;
+  return 0;
 }
 
 // Undeclared experiment hook (scripts only): knock out parts of kernel v2.

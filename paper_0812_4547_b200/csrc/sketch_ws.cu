@@ -36,7 +36,8 @@ constexpr int TILE_BYTES = TILE_WORDS * 4;
 constexpr int NCONS = 256;
 constexpr int NTHREADS = 512;
 
-enum { BAR_FULL0 = 1, BAR_FULL1 = 2, BAR_EMPTY0 = 3, BAR_EMPTY1 = 4, BAR_GRP0 = 5, BAR_GRP1 = 6, BAR_CONS = 7 };
+enum { BAR_FULL0 = 1, BAR_FULL1 = 2, BAR_EMPTY0 = 3, BAR_EMPTY1 = 4, BAR_GRP0 = 5, BAR_GRP1 = 6, BAR_CONS = 7,
+       BAR_TOK0 = 8, BAR_TOK1 = 9 };
 
 // Padded tile layout: row x>>9 of 512 words, rotated by 4*((x>>9)&7) words.
 // Additive over disjoint bit sets, so phys(base + off) = phys(base) + phys(off).
@@ -67,10 +68,14 @@ __device__ __forceinline__ void fwht128(float2 (&v)[64]) {
   }
 }
 
-// Walks this CTA's tiles in order: items blockIdx.x, +gridDim.x, ...; within a
-// slab, sub-blocks in Gray-code order, skipping all-padding ones.
+// Schedule.  A CTA walks items blockIdx.x, +gridDim.x, ... (item = (column, slab)).
+// A slab of cnt tiles is visited as pairs p = 0 .. npairs-1 of tiles
+// j_a = 2 gray(p), j_b = j_a + 1 (Gray code over the tile bits >= 1, so
+// consecutive pairs differ in one k_mid bit >= 1, and the two tiles of a pair
+// differ in k_mid bit 0).  Producer group 0 makes j_a, group 1 makes j_b;
+// tiles with j >= cnt (all padding) are skipped.
 struct Cursor {
-  int it, m, L, cnt, s, col;
+  int it, p, np, cnt, s, col;
   bool valid;
 };
 
@@ -81,30 +86,32 @@ __device__ __forceinline__ void cursor_item(const WsParams& P, Cursor& c) {
   c.s = (int)(c.it - (int64_t)c.col * P.S_act);
   const int64_t j0 = (int64_t)c.s * P.J;
   c.cnt = (int)((P.n_sub - j0 < P.J) ? P.n_sub - j0 : P.J);
-  c.L = 0;
-  while ((1 << c.L) < c.cnt) ++c.L;
-  c.m = 0;
+  int L = 0;
+  while ((1 << L) < c.cnt) ++L;
+  c.np = L ? (1 << (L - 1)) : 1;
+  c.p = 0;
 }
 
-// Advance to the next active tile (gray(m) < cnt).  Returns false when done.
-__device__ __forceinline__ bool cursor_next(const WsParams& P, Cursor& c) {
+__device__ __forceinline__ int pair_tile(const Cursor& c, int g) { return 2 * (c.p ^ (c.p >> 1)) + g; }
+
+// Advance to the next pair whose tile g is active (g = -1: any active pair).
+__device__ __forceinline__ bool cursor_next(const WsParams& P, Cursor& c, int g) {
   while (c.valid) {
-    ++c.m;
-    if (c.m >= (1 << c.L)) {
+    ++c.p;
+    if (c.p >= c.np) {
       c.it += gridDim.x;
       cursor_item(P, c);
       if (!c.valid) return false;
     }
-    if ((c.m ^ (c.m >> 1)) < c.cnt) return true;
+    if (pair_tile(c, g < 0 ? 0 : g) < c.cnt) return true;
   }
   return false;
 }
 
-__device__ __forceinline__ void cursor_start(const WsParams& P, Cursor& c) {
+__device__ __forceinline__ void cursor_start(const WsParams& P, Cursor& c, int g) {
   c.it = blockIdx.x;
   cursor_item(P, c);
-  c.m = -1;
-  cursor_next(P, c);  // gray(0) = 0 < cnt always when valid
+  if (c.valid && pair_tile(c, g < 0 ? 0 : g) >= c.cnt) cursor_next(P, c, g);
 }
 
 __device__ __forceinline__ const float* col_ptr(const WsParams& P, int col) {
@@ -124,6 +131,16 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a16), "r"((bytes - skip) & ~15u) : "memory");
 }
 
+__device__ __forceinline__ void prefetch_pair(const WsParams& P, const Cursor& c, int n) {
+  for (int g = 0; g < 2; ++g) {
+    const int j = pair_tile(c, g);
+    if (j >= c.cnt) continue;
+    const int row0 = (int)(((int64_t)c.s * P.J + j) * B);
+    const int rows = n - row0 < B ? n - row0 : B;
+    prefetch_l2(col_ptr(P, c.col) + row0, (uint32_t)(rows * 4) & ~15u);
+  }
+}
+
 #define TRACE(k)                                                                              \
   if ((DBG & 8) && blockIdx.x == 0 && (p & 31) == 0 && ntr < 64)                             \
     P.trace[((size_t)(g * 4 + wg) * 64 + ntr) * 10 + (k)] = clock64();
@@ -138,23 +155,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
   if (tid < 256) {
     // =========================== producers ===========================
     asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
-    const int g = tid >> 7;                 // producer group == tile buffer
+    const int g = tid >> 7;                 // producer group == tile buffer == tile within a pair
     const int p = tid & 127, lane = p & 31, wg = p >> 5;
     float* tile = tiles + g * TILE_WORDS;
     const int base0 = (lane << 2) + (wg << 7);                                           // phys == identity
     const int base1 = phys((lane & 3) + ((lane >> 2) << 9) + (wg << 12));
     const int n = (int)P.n;
     const bool vec_ok = P.src[0].vec && (P.total_cols == P.ncols0 || P.src[1].vec);
+    // ALT: the two groups alternate their butterfly phases (token barriers
+    // TOK0/TOK1), so one group's shared-memory phases overlap the other's FADD2s.
+    constexpr bool ALT = (DBG & 16) != 0;
+    const int cg = ALT ? -1 : g;  // ALT: both groups walk every active pair
     Cursor cur;
-    cursor_start(P, cur);
-    if (g == 1) cursor_next(P, cur);
+    cursor_start(P, cur, cg);
     int ntr = 0;
+    if (ALT && g == 1) bar_arrive(BAR_TOK0, 256);
     while (cur.valid) {
       TRACE(0)
-      const int row0 = (int)(((int64_t)cur.s * P.J + (cur.m ^ (cur.m >> 1))) * B);
+      const int jt = pair_tile(cur, g);
+      const bool active = jt < cur.cnt;
+      const int row0 = (int)(((int64_t)cur.s * P.J + jt) * B);
       const float* __restrict__ colp = col_ptr(P, cur.col);
-      // advance two tiles for the next iteration (the other group takes the one between)
-      if (cursor_next(P, cur)) cursor_next(P, cur);
+      cursor_next(P, cur, cg);
+      if (ALT && !active) {  // keep the token sequence balanced
+        bar_sync(BAR_TOK1, 256);
+        bar_arrive(BAR_TOK0, 256);
+        bar_sync(BAR_TOK1, 256);
+        bar_arrive(BAR_TOK0, 256);
+        continue;
+      }
       float2 v[64];
       // ---- load D x: element x = v4 + 4*lane + 128*wg + 512*h ----
       const uint4 sgn = __ldg(P.signs_ws + ((size_t)(row0 >> LOG_B) << 7) + p);
@@ -196,7 +225,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
         v[2 * h + 1].y = flipf(v[2 * h + 1].y, (w << (28 - b)) & 0x80000000u);
       }
       TRACE(2)
+      if (ALT) bar_sync(g ? BAR_TOK1 : BAR_TOK0, 256);
       if (!(DBG & 4)) fwht128(v);  // bits 0,1 (vector) and 9..13 (h)
+      if (ALT) bar_arrive(g ? BAR_TOK0 : BAR_TOK1, 256);
       TRACE(3)
       bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);
       TRACE(4)
@@ -216,7 +247,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
         if (acc == 1234.5f) v[0].y = 0.f;
       }
       TRACE(7)
+      if (ALT) bar_sync(g ? BAR_TOK1 : BAR_TOK0, 256);
       if (!(DBG & 4)) fwht128(v);  // bits 2..8
+      if (ALT) bar_arrive(g ? BAR_TOK0 : BAR_TOK1, 256);
       TRACE(8)
 #pragma unroll
       for (int k = 0; k < 64; ++k) {
@@ -228,23 +261,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
       if (DBG & 8) ++ntr;
     }
     bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);  // matches the consumers' last release
+    if (ALT && g == 0) bar_sync(BAR_TOK0, 256);   // matches group 1's initial token
   } else {
     // =========================== consumers ===========================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
     const int c = tid - 256;
     for (int i = c; i < RPT * NCONS; i += NCONS) meta_s[i] = P.meta[i];
-    // L2 prefetch cursor: one thread keeps the HBM stream PREF tiles ahead.
-    constexpr int PREF = 8;
+    // L2 prefetch cursor: one thread keeps the HBM stream PREF pairs ahead.
+    constexpr int PREF = 4;
     Cursor pf;
     const bool pf_thread = (c == 0);
     const int n = (int)P.n;
     if (pf_thread) {
-      cursor_start(P, pf);
+      cursor_start(P, pf, -1);
       for (int k = 0; k < PREF && pf.valid; ++k) {
-        const int row0 = (int)(((int64_t)pf.s * P.J + (pf.m ^ (pf.m >> 1))) * B);
-        const int rows = n - row0 < B ? n - row0 : B;
-        prefetch_l2(col_ptr(P, pf.col) + row0, (uint32_t)(rows * 4) & ~15u);
-        cursor_next(P, pf);
+        prefetch_pair(P, pf, n);
+        cursor_next(P, pf, -1);
       }
     }
     bar_sync(BAR_CONS, NCONS);
@@ -253,8 +285,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
     float acc[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) acc[q] = 0.f;
-    int consumed = 0;
     const uint32_t* mrow = meta_s + c;
+    const char* tb0 = reinterpret_cast<const char*>(tiles);
+    const char* tb1 = tb0 + TILE_BYTES;
     for (int64_t it = blockIdx.x; it < P.n_items; it += gridDim.x) {
       const int col = (int)(it / P.S_act);
       const int s = (int)(it - (int64_t)col * P.S_act);
@@ -262,44 +295,45 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
       const int cnt = (int)((P.n_sub - j0 < P.J) ? P.n_sub - j0 : P.J);
       int L = 0;
       while ((1 << L) < cnt) ++L;
-      for (int m = 0; m < (1 << L); ++m) {
-        const int j = m ^ (m >> 1);
-        const int qb = m ? __ffs(m) - 1 : 0;  // Gray-code bit flipped at step m
-        if (j < cnt) {
-          const int b = consumed & 1;
-          ++consumed;
+      const int np = L ? (1 << (L - 1)) : 1;
+      for (int pp = 0; pp < np; ++pp) {
+        const int ja = 2 * (pp ^ (pp >> 1));
+        const int sh = pp ? __ffs(pp) : 1;  // pair step flips k_mid bit (ctz(pp) + 1): meta bit 31 - sh
+        if (ja < cnt) {
+          const bool both = ja + 1 < cnt;
           if (pf_thread && pf.valid) {
-            const int row0 = (int)(((int64_t)pf.s * P.J + (pf.m ^ (pf.m >> 1))) * B);
-            const int rows = n - row0 < B ? n - row0 : B;
-            prefetch_l2(col_ptr(P, pf.col) + row0, (uint32_t)(rows * 4) & ~15u);
-            cursor_next(P, pf);
+            prefetch_pair(P, pf, n);
+            cursor_next(P, pf, -1);
           }
-          bar_sync(b ? BAR_FULL1 : BAR_FULL0, 384);
-          const char* tb = reinterpret_cast<const char*>(tiles) + b * TILE_BYTES;
+          bar_sync(BAR_FULL0, 384);
+          if (both) bar_sync(BAR_FULL1, 384);
           if (DBG & 2) {
-          } else if (qb == 0) {
+          } else if (both) {
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
               const uint32_t mw = mrow[q * NCONS];
-              const float z = *reinterpret_cast<const float*>(tb + (mw & 0x1ffffu));
-              acc[q] = flipf(acc[q], mw & 0x80000000u) + z;
+              const uint32_t off = mw & 0x1ffffu;
+              const float za = *reinterpret_cast<const float*>(tb0 + off);
+              const float zb = flipf(*reinterpret_cast<const float*>(tb1 + off), mw & 0x80000000u);
+              acc[q] = flipf(acc[q], (mw << sh) & 0x80000000u) + (za + zb);
             }
           } else {
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
               const uint32_t mw = mrow[q * NCONS];
-              const float z = *reinterpret_cast<const float*>(tb + (mw & 0x1ffffu));
-              acc[q] = flipf(acc[q], (mw << qb) & 0x80000000u) + z;
+              const float za = *reinterpret_cast<const float*>(tb0 + (mw & 0x1ffffu));
+              acc[q] = flipf(acc[q], (mw << sh) & 0x80000000u) + za;
             }
           }
-          bar_arrive(b ? BAR_EMPTY1 : BAR_EMPTY0, 384);
+          bar_arrive(BAR_EMPTY0, 384);
+          if (both) bar_arrive(BAR_EMPTY1, 384);
         } else {
 #pragma unroll
-          for (int q = 0; q < RPT; ++q) acc[q] = flipf(acc[q], (mrow[q * NCONS] << qb) & 0x80000000u);
+          for (int q = 0; q < RPT; ++q) acc[q] = flipf(acc[q], (mrow[q * NCONS] << sh) & 0x80000000u);
         }
       }
-      // ---- slab epilogue: undo the frame sign of the last Gray step, write ----
-      const uint32_t jlast = (uint32_t)(((1 << L) - 1) ^ (((1 << L) - 1) >> 1));
+      // ---- slab epilogue: undo the frame sign of the last pair, write ----
+      const uint32_t jlast = (uint32_t)(2 * ((np - 1) ^ ((np - 1) >> 1)));
       const bool second = col >= P.ncols0;
       float* __restrict__ outp = second ? P.src[1].out : P.src[0].out;
       const int64_t ldo = second ? P.src[1].ldo : P.src[0].ldo;
@@ -345,6 +379,12 @@ cudaError_t launch_rpt(const WsParams& wp, int grid, cudaStream_t stream) {
     case 6: return launch_dbg<RPT, 6>(wp, grid, stream);
     case 7: return launch_dbg<RPT, 7>(wp, grid, stream);
     case 8: return launch_dbg<RPT, 8>(wp, grid, stream);
+    case 9: return launch_dbg<RPT, 9>(wp, grid, stream);
+    case 24: return launch_dbg<RPT, 24>(wp, grid, stream);
+    case 25: return launch_dbg<RPT, 25>(wp, grid, stream);
+    case 16: return launch_dbg<RPT, 16>(wp, grid, stream);
+    case 17: return launch_dbg<RPT, 17>(wp, grid, stream);
+    case 20: return launch_dbg<RPT, 20>(wp, grid, stream);
     default: break;
   }
 #endif

@@ -18,7 +18,8 @@ ws = plan.workspace(c)
 out = torch.empty((c, r), device="cuda").t()
 lib = _lib.load()
 res = {}
-for mode in [0, 1, 2, 3, 4, 5, 6, 7]:
+modes = [int(x) for x in sys.argv[4].split(',')] if len(sys.argv) > 4 else [0, 1, 2, 3, 4, 5, 6, 7]
+for mode in modes:
     lib.srht_debug_set_mode(mode)
     for _ in range(3):
         plan.sketch_columns(M, out=out, workspace=ws)
@@ -32,5 +33,7 @@ for mode in [0, 1, 2, 3, 4, 5, 6, 7]:
     lib.srht_profile_stop(arr, 10, ctypes.byref(cnt))
     ms = sum(arr[i] for i in range(cnt.value)) / cnt.value
     res[mode] = (ms, 4.0 * n * c / ms / 1e6)
-    print("mode %d (%s): %.3f ms  %.0f GB/s-equivalent" % (mode, {0: 'full', 1: 'no loads', 2: 'no gather', 3: 'no loads+gather', 4: 'no butterflies', 5: 'no loads+bfly', 6: 'no gather+bfly', 7: 'barriers+smem only'}[mode], ms, res[mode][1]), flush=True)
+    names = {0: 'full', 1: 'no loads', 2: 'no gather', 3: 'no loads+gather', 4: 'no butterflies', 5: 'no loads+bfly',
+             6: 'no gather+bfly', 7: 'barriers+smem only', 16: 'ALT tokens', 17: 'ALT no loads', 20: 'ALT no bfly'}
+    print("mode %d (%s): %.3f ms  %.0f GB/s-equivalent" % (mode, names.get(mode, '?'), ms, res[mode][1]), flush=True)
 lib.srht_debug_set_mode(0)

@@ -19,7 +19,9 @@ out = torch.empty((c, r), device="cuda").t()
 lib = _lib.load()
 tr = torch.zeros(8 * 64 * 10, dtype=torch.int64, device="cuda")
 lib.srht_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
-lib.srht_debug_set_mode(8)
+mode = int(sys.argv[4]) if len(sys.argv) > 4 else 8
+print("trace mode", mode)
+lib.srht_debug_set_mode(mode)
 for _ in range(3):
     plan.sketch_columns(M, out=out, workspace=ws)
 torch.cuda.synchronize()

@@ -223,3 +223,27 @@ def test_invalid_sketch_arguments(lib):
     plan = lib.Plan(100, 1, 10, 0)
     with pytest.raises(lib.SrhtError):
         plan.sketch_columns(torch.zeros((99, 2), device="cuda").t().contiguous().t())
+
+
+@pytest.mark.parametrize("n,r", [(1 << 20, 8192), (1 << 26, 16384), (1 << 18, 5000), (1 << 15, 16384)])
+def test_ws_slot_layout(lib, n, r):
+    # Kernel-v2 consumer slots: every sample exactly once, metadata consistent
+    # with the plan, and each warp-row of 32 gathers at most 2-way bank-conflicted.
+    import ctypes
+    from paper_0812_4547_b200 import _lib
+    plan = lib.Plan(n, 1, r, 3)
+    L = _lib.load()
+    rpt = ctypes.c_int()
+    assert L.srht_debug_copy_ws_layout(plan._h, None, None, ctypes.byref(rpt)) == 0
+    meta = np.empty(rpt.value * 256, dtype=np.uint32)
+    perm = np.empty(rpt.value * 256, dtype=np.int32)
+    assert L.srht_debug_copy_ws_layout(plan._h, meta.ctypes.data, perm.ctypes.data, ctypes.byref(rpt)) == 0
+    valid = perm >= 0
+    assert np.array_equal(np.sort(perm[valid]), np.arange(r))
+    K = plan.indices().astype(np.int64)
+    lo = K[perm[valid]] & ((1 << 14) - 1)
+    phys = (lo & 511) + (((lo >> 9) & 7) << 2) + (lo >> 9) * 544
+    assert np.array_equal(meta[valid] & 0x1FFFF, (phys * 4).astype(np.uint32))
+    banks = np.where(valid, ((meta & 0x1FFFF) // 4 % 32).astype(np.int64), -1).reshape(-1, 32)
+    worst = max(np.bincount(row[row >= 0], minlength=32).max() if (row >= 0).any() else 0 for row in banks)
+    assert worst <= 2, worst
