@@ -74,6 +74,40 @@ __device__ __forceinline__ void fwht128(float2 (&v)[64]) {
 // consecutive pairs differ in one k_mid bit >= 1, and the two tiles of a pair
 // differ in k_mid bit 0).  Producer group 0 makes j_a, group 1 makes j_b;
 // tiles with j >= cnt (all padding) are skipped.
+// The same transform, ordered so that each quarter of the tile (pairs 16q..16q+15)
+// gets its first 5 stages as soon as its own loads land; the 2 stages across
+// quarters (pair strides 16, 32) come last.  Lets the butterflies of quarter 0
+// run while quarters 1-3 are still in flight.
+__device__ __forceinline__ void fwht128_quarter(float2 (&v)[64], int q) {
+#pragma unroll
+  for (int m = 16 * q; m < 16 * q + 16; ++m)
+    v[m] = __ffma2_rn(v[m], make_float2(1.f, -1.f), make_float2(v[m].y, v[m].x));
+#pragma unroll
+  for (int s = 1; s < 16; s <<= 1) {
+#pragma unroll
+    for (int m = 16 * q; m < 16 * q + 16; ++m) {
+      if (!(m & s)) {
+        const float2 a = v[m], b = v[m | s];
+        v[m] = __fadd2_rn(a, b);
+        v[m | s] = __fadd2_rn(a, make_float2(-b.x, -b.y));
+      }
+    }
+  }
+}
+__device__ __forceinline__ void fwht128_cross(float2 (&v)[64]) {
+#pragma unroll
+  for (int s = 16; s < 64; s <<= 1) {
+#pragma unroll
+    for (int m = 0; m < 64; ++m) {
+      if (!(m & s)) {
+        const float2 a = v[m], b = v[m | s];
+        v[m] = __fadd2_rn(a, b);
+        v[m | s] = __fadd2_rn(a, make_float2(-b.x, -b.y));
+      }
+    }
+  }
+}
+
 struct Cursor {
   int it, p, np, cnt, s, col;
   bool valid;
@@ -215,18 +249,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
         if (acc == 1234.5f) v[0].y = 0.f;
       }
       TRACE(1)
-#pragma unroll
-      for (int h = 0; h < 32; ++h) {  // sign of element (h, v) is bit ((h & 7) << 2) + v of word h >> 3
-        const uint32_t w = (h < 8 ? sgn.x : h < 16 ? sgn.y : h < 24 ? sgn.z : sgn.w);
-        const int b = (h & 7) << 2;
-        v[2 * h].x = flipf(v[2 * h].x, (w << (31 - b)) & 0x80000000u);
-        v[2 * h].y = flipf(v[2 * h].y, (w << (30 - b)) & 0x80000000u);
-        v[2 * h + 1].x = flipf(v[2 * h + 1].x, (w << (29 - b)) & 0x80000000u);
-        v[2 * h + 1].y = flipf(v[2 * h + 1].y, (w << (28 - b)) & 0x80000000u);
-      }
       TRACE(2)
       if (ALT) bar_sync(g ? BAR_TOK1 : BAR_TOK0, 256);
-      if (!(DBG & 4)) fwht128(v);  // bits 0,1 (vector) and 9..13 (h)
+      // D (sign XOR) and the butterflies over bits 0,1 (vector) and 9..13 (h),
+      // quarter by quarter in load order.
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const uint32_t w = (qq == 0 ? sgn.x : qq == 1 ? sgn.y : qq == 2 ? sgn.z : sgn.w);
+#pragma unroll
+        for (int h = 8 * qq; h < 8 * qq + 8; ++h) {  // sign of (h, v) = bit ((h & 7) << 2) + v of word h >> 3
+          const int b = (h & 7) << 2;
+          v[2 * h].x = flipf(v[2 * h].x, (w << (31 - b)) & 0x80000000u);
+          v[2 * h].y = flipf(v[2 * h].y, (w << (30 - b)) & 0x80000000u);
+          v[2 * h + 1].x = flipf(v[2 * h + 1].x, (w << (29 - b)) & 0x80000000u);
+          v[2 * h + 1].y = flipf(v[2 * h + 1].y, (w << (28 - b)) & 0x80000000u);
+        }
+        if (!(DBG & 4)) fwht128_quarter(v, qq);
+      }
+      if (!(DBG & 4)) fwht128_cross(v);
       if (ALT) bar_arrive(g ? BAR_TOK0 : BAR_TOK1, 256);
       TRACE(3)
       bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);
@@ -248,7 +288,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
       }
       TRACE(7)
       if (ALT) bar_sync(g ? BAR_TOK1 : BAR_TOK0, 256);
-      if (!(DBG & 4)) fwht128(v);  // bits 2..8
+      if (!(DBG & 4)) {  // bits 2..8, quarter by quarter in LDS order
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) fwht128_quarter(v, qq);
+        fwht128_cross(v);
+      }
       if (ALT) bar_arrive(g ? BAR_TOK0 : BAR_TOK1, 256);
       TRACE(8)
 #pragma unroll
