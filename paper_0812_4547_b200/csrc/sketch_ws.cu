@@ -191,7 +191,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
     asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
     const int g = tid >> 7;                 // producer group == tile buffer == tile within a pair
     const int p = tid & 127, lane = p & 31, wg = p >> 5;
-    float* tile = tiles + g * TILE_WORDS;
     const int base0 = (lane << 2) + (wg << 7);                                           // phys == identity
     const int base1 = phys((lane & 3) + ((lane >> 2) << 9) + (wg << 12));
     const int n = (int)P.n;
@@ -200,12 +199,112 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
     // TOK0/TOK1), so one group's shared-memory phases overlap the other's FADD2s.
     constexpr bool ALT = (DBG & 16) != 0;
     const int cg = ALT ? -1 : g;  // ALT: both groups walk every active pair
+    // SOLO (experiment): group 0 produces every tile, group 1 idles.
+    constexpr bool SOLO = (DBG & 32) != 0;
     Cursor cur;
-    cursor_start(P, cur, cg);
+    cursor_start(P, cur, SOLO ? -1 : cg);
     int ntr = 0;
     if (ALT && g == 1) bar_arrive(BAR_TOK0, 256);
+    auto produce = [&](const int row0, const float* __restrict__ colp, const int bs) {
+      float* tile = tiles + bs * TILE_WORDS;
+        float2 v[64];
+        // ---- load D x: element x = v4 + 4*lane + 128*wg + 512*h ----
+        const uint4 sgn = __ldg(P.signs_ws + ((size_t)(row0 >> LOG_B) << 7) + p);
+        if (DBG & 1) {
+#pragma unroll
+          for (int h = 0; h < 32; ++h) {
+            v[2 * h] = make_float2((float)h, (float)row0);
+            v[2 * h + 1] = make_float2((float)base0, 1.f);
+          }
+        } else if (vec_ok && row0 + B <= n) {
+#pragma unroll
+          for (int h = 0; h < 32; ++h) {
+            const float4 f = __ldcs(reinterpret_cast<const float4*>(colp + row0 + base0 + (h << 9)));
+            v[2 * h] = make_float2(f.x, f.y);
+            v[2 * h + 1] = make_float2(f.z, f.w);
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 32; ++h) {
+            const int row = row0 + base0 + (h << 9);
+            v[2 * h] = make_float2(row + 0 < n ? colp[row + 0] : 0.f, row + 1 < n ? colp[row + 1] : 0.f);
+            v[2 * h + 1] = make_float2(row + 2 < n ? colp[row + 2] : 0.f, row + 3 < n ? colp[row + 3] : 0.f);
+          }
+        }
+        if (DBG & 8) {
+          float acc = 0.f;
+#pragma unroll
+          for (int h = 0; h < 64; ++h) acc += v[h].x;
+          if (acc == 1234.5f) v[0].y = 0.f;
+        }
+        TRACE(1)
+        TRACE(2)
+        if (ALT) bar_sync(g ? BAR_TOK1 : BAR_TOK0, 256);
+        // D (sign XOR) and the butterflies over bits 0,1 (vector) and 9..13 (h),
+        // quarter by quarter in load order.
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          const uint32_t w = (qq == 0 ? sgn.x : qq == 1 ? sgn.y : qq == 2 ? sgn.z : sgn.w);
+#pragma unroll
+          for (int h = 8 * qq; h < 8 * qq + 8; ++h) {  // sign of (h, v) = bit ((h & 7) << 2) + v of word h >> 3
+            const int b = (h & 7) << 2;
+            v[2 * h].x = flipf(v[2 * h].x, (w << (31 - b)) & 0x80000000u);
+            v[2 * h].y = flipf(v[2 * h].y, (w << (30 - b)) & 0x80000000u);
+            v[2 * h + 1].x = flipf(v[2 * h + 1].x, (w << (29 - b)) & 0x80000000u);
+            v[2 * h + 1].y = flipf(v[2 * h + 1].y, (w << (28 - b)) & 0x80000000u);
+          }
+          if (!(DBG & 4)) fwht128_quarter(v, qq);
+        }
+        if (!(DBG & 4)) fwht128_cross(v);
+        if (ALT) bar_arrive(g ? BAR_TOK0 : BAR_TOK1, 256);
+        TRACE(3)
+        bar_sync(bs ? BAR_EMPTY1 : BAR_EMPTY0, 384);
+        TRACE(4)
+#pragma unroll
+        for (int h = 0; h < 32; ++h)
+          *reinterpret_cast<float4*>(tile + base0 + ((h & 7) << 2) + h * ROW) =
+              make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y);
+        TRACE(5)
+        bar_sync(g ? BAR_GRP1 : BAR_GRP0, 128);
+        TRACE(6)
+#pragma unroll
+        for (int k = 0; k < 64; ++k) v[k] = make_float2(tile[base1 + 8 * k], tile[base1 + 8 * k + 4]);
+        if (DBG & 8) {
+          float acc = 0.f;
+#pragma unroll
+          for (int h = 0; h < 64; ++h) acc += v[h].x;
+          if (acc == 1234.5f) v[0].y = 0.f;
+        }
+        TRACE(7)
+        if (ALT) bar_sync(g ? BAR_TOK1 : BAR_TOK0, 256);
+        if (!(DBG & 4)) {  // bits 2..8, quarter by quarter in LDS order
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) fwht128_quarter(v, qq);
+          fwht128_cross(v);
+        }
+        if (ALT) bar_arrive(g ? BAR_TOK0 : BAR_TOK1, 256);
+        TRACE(8)
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          tile[base1 + 8 * k] = v[k].x;
+          tile[base1 + 8 * k + 4] = v[k].y;
+        }
+        bar_arrive(bs ? BAR_FULL1 : BAR_FULL0, 384);
+        TRACE(9)
+        if (DBG & 8) ++ntr;
+    };
+    if (SOLO && g == 1) cur.valid = false;
     while (cur.valid) {
       TRACE(0)
+      if (SOLO) {
+        const Cursor c0 = cur;
+        cursor_next(P, cur, -1);
+        for (int sub = 0; sub < 2; ++sub) {
+          const int jt = pair_tile(c0, sub);
+          if (jt < c0.cnt) produce((int)(((int64_t)c0.s * P.J + jt) * B), col_ptr(P, c0.col), sub);
+        }
+        continue;
+      }
       const int jt = pair_tile(cur, g);
       const bool active = jt < cur.cnt;
       const int row0 = (int)(((int64_t)cur.s * P.J + jt) * B);
@@ -218,93 +317,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
         bar_arrive(BAR_TOK0, 256);
         continue;
       }
-      float2 v[64];
-      // ---- load D x: element x = v4 + 4*lane + 128*wg + 512*h ----
-      const uint4 sgn = __ldg(P.signs_ws + ((size_t)(row0 >> LOG_B) << 7) + p);
-      if (DBG & 1) {
-#pragma unroll
-        for (int h = 0; h < 32; ++h) {
-          v[2 * h] = make_float2((float)h, (float)row0);
-          v[2 * h + 1] = make_float2((float)base0, 1.f);
-        }
-      } else if (vec_ok && row0 + B <= n) {
-#pragma unroll
-        for (int h = 0; h < 32; ++h) {
-          const float4 f = __ldcs(reinterpret_cast<const float4*>(colp + row0 + base0 + (h << 9)));
-          v[2 * h] = make_float2(f.x, f.y);
-          v[2 * h + 1] = make_float2(f.z, f.w);
-        }
-      } else {
-#pragma unroll
-        for (int h = 0; h < 32; ++h) {
-          const int row = row0 + base0 + (h << 9);
-          v[2 * h] = make_float2(row + 0 < n ? colp[row + 0] : 0.f, row + 1 < n ? colp[row + 1] : 0.f);
-          v[2 * h + 1] = make_float2(row + 2 < n ? colp[row + 2] : 0.f, row + 3 < n ? colp[row + 3] : 0.f);
-        }
-      }
-      if (DBG & 8) {
-        float acc = 0.f;
-#pragma unroll
-        for (int h = 0; h < 64; ++h) acc += v[h].x;
-        if (acc == 1234.5f) v[0].y = 0.f;
-      }
-      TRACE(1)
-      TRACE(2)
-      if (ALT) bar_sync(g ? BAR_TOK1 : BAR_TOK0, 256);
-      // D (sign XOR) and the butterflies over bits 0,1 (vector) and 9..13 (h),
-      // quarter by quarter in load order.
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const uint32_t w = (qq == 0 ? sgn.x : qq == 1 ? sgn.y : qq == 2 ? sgn.z : sgn.w);
-#pragma unroll
-        for (int h = 8 * qq; h < 8 * qq + 8; ++h) {  // sign of (h, v) = bit ((h & 7) << 2) + v of word h >> 3
-          const int b = (h & 7) << 2;
-          v[2 * h].x = flipf(v[2 * h].x, (w << (31 - b)) & 0x80000000u);
-          v[2 * h].y = flipf(v[2 * h].y, (w << (30 - b)) & 0x80000000u);
-          v[2 * h + 1].x = flipf(v[2 * h + 1].x, (w << (29 - b)) & 0x80000000u);
-          v[2 * h + 1].y = flipf(v[2 * h + 1].y, (w << (28 - b)) & 0x80000000u);
-        }
-        if (!(DBG & 4)) fwht128_quarter(v, qq);
-      }
-      if (!(DBG & 4)) fwht128_cross(v);
-      if (ALT) bar_arrive(g ? BAR_TOK0 : BAR_TOK1, 256);
-      TRACE(3)
-      bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);
-      TRACE(4)
-#pragma unroll
-      for (int h = 0; h < 32; ++h)
-        *reinterpret_cast<float4*>(tile + base0 + ((h & 7) << 2) + h * ROW) =
-            make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y);
-      TRACE(5)
-      bar_sync(g ? BAR_GRP1 : BAR_GRP0, 128);
-      TRACE(6)
-#pragma unroll
-      for (int k = 0; k < 64; ++k) v[k] = make_float2(tile[base1 + 8 * k], tile[base1 + 8 * k + 4]);
-      if (DBG & 8) {
-        float acc = 0.f;
-#pragma unroll
-        for (int h = 0; h < 64; ++h) acc += v[h].x;
-        if (acc == 1234.5f) v[0].y = 0.f;
-      }
-      TRACE(7)
-      if (ALT) bar_sync(g ? BAR_TOK1 : BAR_TOK0, 256);
-      if (!(DBG & 4)) {  // bits 2..8, quarter by quarter in LDS order
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) fwht128_quarter(v, qq);
-        fwht128_cross(v);
-      }
-      if (ALT) bar_arrive(g ? BAR_TOK0 : BAR_TOK1, 256);
-      TRACE(8)
-#pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        tile[base1 + 8 * k] = v[k].x;
-        tile[base1 + 8 * k + 4] = v[k].y;
-      }
-      bar_arrive(g ? BAR_FULL1 : BAR_FULL0, 384);
-      TRACE(9)
-      if (DBG & 8) ++ntr;
+      produce(row0, colp, g);
     }
-    bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);  // matches the consumers' last release
+    if (SOLO) {
+      if (g == 0) {
+        bar_sync(BAR_EMPTY0, 384);
+        bar_sync(BAR_EMPTY1, 384);
+      }
+    } else {
+      bar_sync(g ? BAR_EMPTY1 : BAR_EMPTY0, 384);  // matches the consumers' last release
+    }
     if (ALT && g == 0) bar_sync(BAR_TOK0, 256);   // matches group 1's initial token
   } else {
     // =========================== consumers ===========================
@@ -427,6 +449,9 @@ cudaError_t launch_rpt(const WsParams& wp, int grid, cudaStream_t stream) {
     case 24: return launch_dbg<RPT, 24>(wp, grid, stream);
     case 25: return launch_dbg<RPT, 25>(wp, grid, stream);
     case 16: return launch_dbg<RPT, 16>(wp, grid, stream);
+    case 32: return launch_dbg<RPT, 32>(wp, grid, stream);
+    case 33: return launch_dbg<RPT, 33>(wp, grid, stream);
+    case 35: return launch_dbg<RPT, 35>(wp, grid, stream);
     case 17: return launch_dbg<RPT, 17>(wp, grid, stream);
     case 20: return launch_dbg<RPT, 20>(wp, grid, stream);
     default: break;

@@ -34,6 +34,6 @@ for mode in modes:
     ms = sum(arr[i] for i in range(cnt.value)) / cnt.value
     res[mode] = (ms, 4.0 * n * c / ms / 1e6)
     names = {0: 'full', 1: 'no loads', 2: 'no gather', 3: 'no loads+gather', 4: 'no butterflies', 5: 'no loads+bfly',
-             6: 'no gather+bfly', 7: 'barriers+smem only', 16: 'ALT tokens', 17: 'ALT no loads', 20: 'ALT no bfly'}
+             6: 'no gather+bfly', 7: 'barriers+smem only', 16: 'ALT tokens', 17: 'ALT no loads', 20: 'ALT no bfly', 32: 'SOLO group', 33: 'SOLO no loads', 35: 'SOLO no loads/gather'}
     print("mode %d (%s): %.3f ms  %.0f GB/s-equivalent" % (mode, names.get(mode, '?'), ms, res[mode][1]), flush=True)
 lib.srht_debug_set_mode(0)

@@ -132,3 +132,23 @@ def test_config5_full_sampled_columns(lib):
         assert_tol(SMh[:, j:j + 1], ref, col[:, None])
     del M
     torch.cuda.empty_cache()
+
+
+def test_config4_end_to_end_nnls(lib):
+    # Reading R14 at full config-4 size: Lawson-Hanson on the GPU sketch and on
+    # the oracle sketch, R(x~) on the original 2^20 x 512 data, within 1e-6.
+    import torch
+    from oracle import srht as osr
+    c = workloads.CONFIGS[4]
+    n, d, r = c["n"], c["d"], c["r"]
+    M, _ = workloads.dense_device(n, d, seed=workloads.SEED)
+    plan = lib.Plan(n, d, r, workloads.SEED)
+    SM = plan.sketch_columns(M, workspace=plan.workspace(d + 1)).cpu().numpy().astype(np.float64)
+    Mh = M.cpu().numpy()
+    del M
+    torch.cuda.empty_cache()
+    ref = np.empty((r, d + 1))
+    for j0 in range(0, d + 1, 32):
+        ref[:, j0:j0 + 32] = osr.sketch(Mh[:, j0:j0 + 32].astype(np.float64), workloads.SEED, r)
+    assert_tol(SM, ref, Mh)
+    e2e_gate(Mh[:, :d].astype(np.float64), Mh[:, d].astype(np.float64), SM[:, :d], SM[:, d], ref[:, :d], ref[:, d])
