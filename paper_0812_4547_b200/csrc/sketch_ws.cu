@@ -446,10 +446,14 @@ cudaError_t launch_rpt(const WsParams& wp, int grid, cudaStream_t stream) {
     case 7: return launch_dbg<RPT, 7>(wp, grid, stream);
     case 8: return launch_dbg<RPT, 8>(wp, grid, stream);
     case 9: return launch_dbg<RPT, 9>(wp, grid, stream);
+    case 11: return launch_dbg<RPT, 11>(wp, grid, stream);
     case 24: return launch_dbg<RPT, 24>(wp, grid, stream);
     case 25: return launch_dbg<RPT, 25>(wp, grid, stream);
     case 16: return launch_dbg<RPT, 16>(wp, grid, stream);
     case 32: return launch_dbg<RPT, 32>(wp, grid, stream);
+    case 40: return launch_dbg<RPT, 40>(wp, grid, stream);
+    case 41: return launch_dbg<RPT, 41>(wp, grid, stream);
+    case 43: return launch_dbg<RPT, 43>(wp, grid, stream);
     case 33: return launch_dbg<RPT, 33>(wp, grid, stream);
     case 35: return launch_dbg<RPT, 35>(wp, grid, stream);
     case 17: return launch_dbg<RPT, 17>(wp, grid, stream);
