@@ -70,15 +70,23 @@ def load_peaks():
         return 6650.0, "fallback", {}
 
 
-def load_traffic(config):
+def load_traffic(config, kernel):
     """dram read+write bytes per launch of the tile kernel from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("config%d" % config)
+        return d.get(kernel, {}).get("config%d" % config)
     except Exception:
         return None
+
+
+KERNEL_NAMES = {1: "k_sketch_tiles", 2: "k_sketch_ws", 3: "k_sketch_tma"}
+
+
+def last_kernel(lib):
+    """Name of the tile kernel the library ran for the last sketch call."""
+    return KERNEL_NAMES.get(lib.srht_debug_last_kernel(), "unknown")
 
 
 class ClockSampler:
@@ -310,11 +318,12 @@ def main():
 
     total_in = 4.0 * n * c
     value = total_in / (ms * 1e-3) / 1e9
+    kname = last_kernel(lib)
     peak, peak_kind, peaks = load_peaks()
     alg_bytes_launch = 4.0 * n * cl + 4.0 * r * cl  # read the shard once, write r x c_l
     achieved = alg_bytes_launch / (kms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(args.config), "kernel": "k_sketch_ws" if plan.N >= 16384 and r <= 16384 else "k_sketch_tiles",
+                "traffic": load_traffic(args.config, kname), "kernel": kname,
                 "peak_source": "%s (MEASURED_PEAKS.json hbm_gbs)" % peak_kind if peak_kind == "measured"
                 else "fallback 6650 GB/s (B200_PROFILING.md)",
                 "kernel_ms": kms, "share_of_step": kms / ms}

@@ -70,6 +70,9 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    # Experiment switch: SRHT_KERNEL=v2 runs kernel v2 where kernel v3 would (A/B runs).
+    if os.environ.get("SRHT_KERNEL") == "v2":
+        lib.srht_debug_set_kernel(2)
     _lib = lib
     return lib
 

@@ -58,56 +58,89 @@ size_t partial_bytes(const srht_plan* P, int64_t ncols) {
   return (b + 255) & ~size_t(255);
 }
 
-// Kernel v2 consumer slot layout (host side, once per plan).  Sample t goes to
-// slot (q, c): consumer thread c = 32*w + lane reads meta[q*256 + c].  Rows
-// (q, w) of 32 lanes take at most one sample per shared-memory bank of
-// phys(k_lo) where possible, so the gather LDS is conflict-free.
-cudaError_t build_ws_layout(srht_plan* P) {
-  const int64_t r = P->r;
-  const int rows = P->rpt2 * 8;
-  const int slots = P->rpt2 * 256;
-  std::vector<int32_t> K(r);
-  cudaError_t e = cudaMemcpy(K.data(), P->d_K, r * sizeof(int32_t), cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return e;
+// Consumer slot layout (host side, once per plan) shared by kernels v2 and v3.
+// Sample t goes to slot (q, c): consumer thread c = 32*w + lane handles it as its
+// q-th accumulator.  Rows (q, w) of 32 lanes take at most one sample per
+// shared-memory bank of the gather address where possible, so the gather LDS is
+// conflict-free.  Samples, sorted by bank, are dealt round-robin over the rows:
+// sample i of the bank-sorted order goes to row i mod rows, so a bank with c samples
+// lands in min(c, rows) distinct rows (<= ceil(max_c / rows) per row).
+// Returns slot_t[q*256 + 32*w + lane] = t or -1.
+std::vector<int32_t> deal_slots(const std::vector<int32_t>& K, int rpt, int (*addr)(int)) {
+  const int rows = rpt * 8;
+  const int slots = rpt * 256;
   std::vector<std::vector<int32_t>> bucket(32);
-  for (int64_t t = 0; t < r; ++t) {
-    const int lo = K[t] & ((1 << 14) - 1);
-    bucket[srht::ws_phys(lo) & 31].push_back((int32_t)t);
-  }
-  // Deal the samples, sorted by bank, round-robin over the rows: sample i of the
-  // bank-sorted order goes to row i mod rows.  A bank with c samples then lands
-  // in min(c, rows) distinct rows, so a row holds at most ceil(max_c / rows)
-  // samples of one bank (1 when every bank has <= rows samples, 2 otherwise).
-  std::vector<int32_t> slot_t(slots, -1);
+  for (size_t t = 0; t < K.size(); ++t) bucket[addr(K[t] & ((1 << 14) - 1)) & 31].push_back((int32_t)t);
+  std::vector<int32_t> row_t(slots, -1);
   std::vector<int> fill(rows, 0);
   int64_t i = 0;
   for (int b = 0; b < 32; ++b)
     for (int32_t t : bucket[b]) {
       const int row = (int)(i % rows);
-      slot_t[row * 32 + fill[row]++] = t;
+      row_t[row * 32 + fill[row]++] = t;
       ++i;
     }
-  // row = q*8 + w, lane = bank  ->  meta index q*256 + 32*w + lane
-  std::vector<uint32_t> meta(slots, 0u);
-  std::vector<int32_t> perm(slots, -1);
+  std::vector<int32_t> slot_t(slots, -1);  // row = q*8 + w, lane -> index q*256 + 32*w + lane
   for (int row = 0; row < rows; ++row)
-    for (int lane = 0; lane < 32; ++lane) {
-      const int32_t t = slot_t[row * 32 + lane];
-      const int q = row / 8, w = row % 8;
-      const int idx = q * 256 + w * 32 + lane;
-      perm[idx] = t;
+    for (int lane = 0; lane < 32; ++lane) slot_t[(row / 8) * 256 + (row % 8) * 32 + lane] = row_t[row * 32 + lane];
+  return slot_t;
+}
+
+template <typename T>
+cudaError_t upload(T** dst, const std::vector<T>& v) {
+  cudaError_t e = cudaMalloc(dst, v.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+// Kernel v2: meta = byte offset of phys(k_lo) | reversed k_mid bits at the top.
+cudaError_t build_ws_layout(srht_plan* P, const std::vector<int32_t>& K) {
+  const int slots = P->rpt2 * 256;
+  const std::vector<int32_t> slot_t = deal_slots(K, P->rpt2, srht::ws_phys);
+  std::vector<uint32_t> meta(slots, 0u);
+  for (int idx = 0; idx < slots; ++idx) {
+    const int32_t t = slot_t[idx];
+    if (t < 0) continue;
+    const int k = K[t];
+    const uint32_t off = (uint32_t)srht::ws_phys(k & ((1 << 14) - 1)) * 4u;
+    const uint32_t kmid = (uint32_t)(k >> 14) & (uint32_t)(P->J2 - 1);
+    uint32_t rev = 0;
+    for (int i = 0; i < P->log_j2; ++i) rev |= ((kmid >> i) & 1u) << (31 - i);
+    meta[idx] = off | rev;
+  }
+  cudaError_t e = upload(&P->d_meta, meta);
+  if (e == cudaSuccess) e = upload(&P->d_perm, slot_t);
+  return e;
+}
+
+// Kernel v3: per consumer thread c, rpt2/2 words of two 15-bit mid-layout word
+// offsets (slot q = 2i in bits 0..14, 2i+1 in bits 17..31 of word i); perm =
+// t | k_mid << 16; masks[sh][c] bit q = bit sh of k_mid of slot (q, c).
+cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
+  const int rpt = P->rpt2, slots = rpt * 256, mw = rpt / 2;
+  const std::vector<int32_t> slot_t = deal_slots(K, rpt, srht::v3_mid);
+  std::vector<uint32_t> meta((size_t)256 * mw, 0u);
+  std::vector<int32_t> perm(slots, -1);
+  std::vector<uint2> masks((size_t)(P->log_j2 > 0 ? P->log_j2 : 1) * 256, make_uint2(0u, 0u));
+  for (int q = 0; q < rpt; ++q)
+    for (int c = 0; c < 256; ++c) {
+      const int32_t t = slot_t[q * 256 + c];
       if (t < 0) continue;
       const int k = K[t];
-      const uint32_t off = (uint32_t)srht::ws_phys(k & ((1 << 14) - 1)) * 4u;
+      const uint32_t off = (uint32_t)srht::v3_mid(k & ((1 << 14) - 1));
       const uint32_t kmid = (uint32_t)(k >> 14) & (uint32_t)(P->J2 - 1);
-      uint32_t rev = 0;
-      for (int i = 0; i < P->log_j2; ++i) rev |= ((kmid >> i) & 1u) << (31 - i);
-      meta[idx] = off | rev;
+      meta[(size_t)c * mw + q / 2] |= off << (17 * (q & 1));  // lo | hi << 17
+      perm[q * 256 + c] = t | (int32_t)(kmid << 16);
+      for (int sh = 0; sh < P->log_j2; ++sh)
+        if ((kmid >> sh) & 1u) {
+          uint2& m = masks[(size_t)sh * 256 + c];
+          if (q < 32) m.x |= 1u << q; else m.y |= 1u << (q - 32);
+        }
     }
-  if ((e = cudaMalloc(&P->d_meta, slots * sizeof(uint32_t))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&P->d_perm, slots * sizeof(int32_t))) != cudaSuccess) return e;
-  if ((e = cudaMemcpy(P->d_meta, meta.data(), slots * sizeof(uint32_t), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-  return cudaMemcpy(P->d_perm, perm.data(), slots * sizeof(int32_t), cudaMemcpyHostToDevice);
+  cudaError_t e = upload(&P->d_meta3, meta);
+  if (e == cudaSuccess) e = upload(&P->d_perm3, perm);
+  if (e == cudaSuccess) e = upload(&P->d_masks3, masks);
+  return e;
 }
 
 srht::SketchParams base_params(const srht_plan* P) {
@@ -124,6 +157,7 @@ srht::SketchParams base_params(const srht_plan* P) {
   sp.S_act = P->S_act;
   sp.groups = P->groups;
   sp.scale = P->scale;
+  sp.scale_f64 = 1.0 / std::sqrt((double)P->r);
   return sp;
 }
 
@@ -152,7 +186,54 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       cudaError_t e = srht::launch_sketch(P, sp, st);
       return e == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
     }
-    if (nd) {
+    bool v3 = nd && P->v3_ok && srht::g_kernel_force != 2;
+    for (int i = 0; i < nd; ++i) v3 = v3 && dense[i].vec;
+    int64_t ncol_all = 0;
+    for (int i = 0; i < nd; ++i) ncol_all += dense[i].ncols;
+    v3 = v3 && ncol_all * P->S_act2 < (int64_t(1) << 31);
+    if (v3) {
+      srht::V3Params vp;
+      std::memset(&vp, 0, sizeof(vp));
+      vp.src[0] = dense[0];
+      vp.ncols0 = dense[0].ncols;
+      vp.total_cols = dense[0].ncols;
+      if (nd == 2) {
+        vp.src[1] = dense[1];
+        vp.total_cols += dense[1].ncols;
+      }
+      vp.signs = P->d_signs3;
+      vp.meta = P->d_meta3;
+      vp.perm = P->d_perm3;
+      vp.masks = P->d_masks3;
+      vp.log_j = P->log_j2;
+      vp.r = P->r;
+      vp.n = P->n;
+      vp.J = P->J2;
+      vp.n_sub = P->n_sub2;
+      vp.S_act = P->S_act2;
+      vp.n_items = vp.total_cols * P->S_act2;
+      vp.n_items32 = (int)vp.n_items;
+      vp.S_act32 = (int)vp.S_act;
+      vp.J32 = (int)vp.J;
+      vp.n_sub32 = (int)vp.n_sub;
+      vp.scale = P->scale;
+      vp.partials = sp.partials;
+      const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
+      if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
+      cudaError_t e = srht::launch_sketch_tma(P, vp, st);
+      srht::g_last_kernel = 3;
+      if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot + 1], st);
+      if (e != cudaSuccess) return SRHT_ECUDA;
+      if (P->S_act2 > 1) {
+        srht::SketchParams rp = sp;
+        rp.src[0] = vp.src[0];
+        rp.src[1] = vp.src[1];
+        rp.ncols0 = vp.ncols0;
+        rp.total_cols = vp.total_cols;
+        rp.S_act = P->S_act2;
+        if (srht::launch_reduce(rp, 14 + P->log_j2, st) != cudaSuccess) return SRHT_ECUDA;
+      }
+    } else if (nd) {
       srht::WsParams wp;
       std::memset(&wp, 0, sizeof(wp));
       wp.src[0] = dense[0];
@@ -178,6 +259,7 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
       if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
       cudaError_t e = srht::launch_sketch_ws(P, wp, st);
+      srht::g_last_kernel = 2;
       if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot + 1], st);
       if (e != cudaSuccess) return SRHT_ECUDA;
       if (P->S_act2 > 1) {
@@ -301,17 +383,23 @@ srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t s
     P->n_sub2 = (n + (1 << 14) - 1) >> 14;
     P->S_act2 = (P->n_sub2 + P->J2 - 1) / P->J2;
     P->rpt2 = r <= 8 * 256 ? 8 : r <= 16 * 256 ? 16 : r <= 32 * 256 ? 32 : 64;
-    e = build_ws_layout(P);
+    std::vector<int32_t> K(r);
+    e = cudaMemcpy(K.data(), P->d_K, r * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = build_ws_layout(P, K);
+    if (e == cudaSuccess) e = build_v3_layout(P, K);
     const int64_t n_tiles = (P->N_eff >> 14);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_signs_ws, n_tiles * 128 * sizeof(uint4));
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_signs3, n_tiles * 128 * sizeof(uint4));
     if (e == cudaSuccess) {
       cudaStream_t st2;
       e = cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking);
       if (e == cudaSuccess) {
         e = srht::build_ws_signs(P->d_signs, n_tiles, P->d_signs_ws, st2);
+        if (e == cudaSuccess) e = srht::build_v3_signs(P->d_signs, n_tiles, P->d_signs3, st2);
         cudaStreamDestroy(st2);
       }
     }
+    P->v3_ok = (e == cudaSuccess) && P->log_j2 <= srht::V3_MAX_LOGJ;
   }
   if (e != cudaSuccess) {
     srht_plan_destroy(P);
@@ -332,6 +420,10 @@ srht_status srht_plan_destroy(srht_plan* P) {
   cudaFree(P->d_meta);
   cudaFree(P->d_perm);
   cudaFree(P->d_signs_ws);
+  cudaFree(P->d_signs3);
+  cudaFree(P->d_meta3);
+  cudaFree(P->d_perm3);
+  cudaFree(P->d_masks3);
   delete P;
   return SRHT_OK;
 }
@@ -424,6 +516,13 @@ int srht_debug_copy_ws_layout(const srht_plan* P, uint32_t* meta, int32_t* perm,
 // bit2: producers skip the butterflies.  Results are wrong when non-zero.
 int srht_debug_set_mode(int mode) {
   srht::g_debug_mode = mode;
+  return 0;
+}
+// Undeclared experiment hook: 0 = automatic kernel choice, 2 = use kernel v2 where
+// kernel v3 would run (A/B comparison in scripts and tests).
+int srht_debug_last_kernel(void) { return srht::g_last_kernel; }
+int srht_debug_set_kernel(int version) {
+  srht::g_kernel_force = version;
   return 0;
 }
 int srht_debug_set_trace(unsigned long long* dev_buf) {

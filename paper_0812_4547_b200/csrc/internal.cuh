@@ -32,6 +32,12 @@ struct srht_plan {
   uint4* d_signs_ws;  // [N/2^14][128] sign bits in producer-thread order
   uint32_t* d_meta;   // [rpt2*256]: byte offset of phys(k_lo) | reversed k_mid << 17
   int32_t* d_perm;    // [rpt2*256]: sample index t or -1
+  // Kernel v3 (TMA-fed, same geometry as v2): layouts for its own tile order.
+  bool v3_ok;
+  uint4* d_signs3;    // [N/2^14][128] sign bits of rows e + 2p + 256h, bit 2h+e
+  uint32_t* d_meta3;  // [256][rpt2/2]: two 16-bit mid-layout word offsets per word
+  int32_t* d_perm3;   // [rpt2][256]: t | k_mid << 16, or -1
+  uint2* d_masks3;    // [log_j2][256]: bit q = bit sh of k_mid of slot (q, c)
 };
 
 namespace srht {
@@ -39,6 +45,7 @@ namespace srht {
 // Plan builder (plan.cu): fills d_signs and d_K; synchronous on `stream`.
 cudaError_t build_plan_device(srht_plan* P, cudaStream_t stream);
 cudaError_t build_ws_signs(const uint64_t* signs, int64_t n_tiles, uint4* out, cudaStream_t stream);
+cudaError_t build_v3_signs(const uint64_t* signs, int64_t n_tiles, uint4* out, cudaStream_t stream);
 
 // One column source of a sketch launch.
 struct ColSrc {
@@ -69,6 +76,7 @@ struct SketchParams {
   int64_t S_act;
   int64_t groups;
   float scale;
+  double scale_f64;           // r^{-1/2} in FP64 (slab reduction)
   float* partials;            // [S_act][total_cols][r] when S_act > 1
 };
 
@@ -93,7 +101,28 @@ extern int g_debug_mode;
 extern unsigned long long* g_debug_trace;
 cudaError_t launch_sketch_ws(const srht_plan* P, const WsParams& wp, cudaStream_t stream);
 int ws_phys(int x);  // tile layout of kernel v2 (host side, for the slot layout)
-// Fixed-order slab reduction shared by both kernels.
+// Kernel v3 (sketch_tma.cu): dense columns with 16-byte aligned columns (TMA bulk copies).
+constexpr int V3_MAX_LOGJ = 6;
+struct V3Params {
+  ColSrc src[2];
+  int64_t ncols0, total_cols;
+  const uint4* signs;     // plan d_signs3
+  const uint32_t* meta;   // plan d_meta3
+  const int32_t* perm;    // plan d_perm3
+  const uint2* masks;     // plan d_masks3
+  int log_j;
+  int64_t r, n;
+  int64_t J, n_sub, S_act;
+  int64_t n_items;        // total_cols * S_act
+  int n_items32, S_act32, J32, n_sub32;  // the same, 32-bit (checked on the host)
+  float scale;
+  float* partials;        // [S_act][total_cols][r] when S_act > 1
+};
+cudaError_t launch_sketch_tma(const srht_plan* P, const V3Params& vp, cudaStream_t stream);
+int v3_mid(int x);  // kernel-v3 z layout (host side, for the slot layout)
+extern int g_kernel_force;  // 0 auto, 2 = kernel v2 instead of v3 (srht_debug_set_kernel)
+extern int g_last_kernel;   // 1/2/3: tile kernel of the last srht_sketch* call (bench labels)
+// Fixed-order slab reduction shared by every kernel.
 cudaError_t launch_reduce(const SketchParams& sp, int slab_shift, cudaStream_t stream);
 
 // Profiling (srht_profile_start/stop): event pairs around the tile kernel.

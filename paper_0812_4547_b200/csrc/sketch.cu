@@ -278,15 +278,17 @@ __global__ void k_reduce_slabs(const __grid_constant__ SketchParams P, int slab_
   if (t >= P.r || col >= P.total_cols) return;
   const int64_t prob = col / P.cols_per_problem;
   const uint32_t ks = (uint32_t)(P.K[prob * P.r + t] >> slab_shift);
-  float sum = 0.f;
+  // FP32 slab partials, summed in FP64 (fixed order) and scaled by r^{-1/2} once
+  // before the single rounding to FP32 (reading R10).
+  double sum = 0.0;
   for (int64_t s = 0; s < P.S_act; ++s) {
     const float v = P.partials[(s * P.total_cols + col) * P.r + t];
-    sum += flip(v, __popc(ks & (uint32_t)s) & 1u);
+    sum += (double)flip(v, __popc(ks & (uint32_t)s) & 1u);
   }
   const bool second = col >= P.ncols0;
   const ColSrc& cs = second ? P.src[1] : P.src[0];
   const int64_t lc = second ? col - P.ncols0 : col;
-  cs.out[lc * cs.ldo + t] = sum * P.scale;
+  cs.out[lc * cs.ldo + t] = (float)(sum * P.scale_f64);
 }
 
 template <int LOG_B, int RPT>
@@ -324,6 +326,8 @@ cudaError_t launch_b(int rpt, const SketchParams& sp, int64_t items, cudaStream_
 
 ProfileState g_prof;
 int g_debug_mode = 0;
+int g_kernel_force = 0;
+int g_last_kernel = 0;
 unsigned long long* g_debug_trace = nullptr;
 
 cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream_t stream) {
@@ -341,6 +345,7 @@ cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream
     default: return cudaErrorInvalidValue;
   }
   if (slot >= 0) cudaEventRecord(g_prof.ev[2 * slot + 1], stream);
+  g_last_kernel = 1;
   if (e != cudaSuccess || sp.S_act == 1) return e;
   return launch_reduce(sp, P->log_b + P->log_j, stream);
 }

@@ -1,0 +1,407 @@
+// Kernel v3: TMA-fed, warp-specialized SRHT tile kernel for dense FP32 columns (sm_100a).
+//
+// Same decomposition as kernels v1/v2 (Ailon-Liberty pruning):
+//   SM[t] = r^{-1/2} sum_slab (-1)^{popc(k_slab & s)} sum_j (-1)^{popc(k_mid & j)} (H_B D x_{s,j})[k_lo]
+// with B = 2^14 rows per tile.  What changes against v2:
+//
+//  * Tiles arrive by TMA bulk copy (cp.async.bulk, 64 KB per tile) into a ring of
+//    three shared-memory buffers.  Measured on B200 (profiles/r01_mb_l1_sharing.txt):
+//    a TMA fill does not take shared-memory bandwidth from LDS/STS, while an LDG
+//    stream costs ~1.3 crossbar words per word loaded.  The HBM latency also
+//    leaves the producers' critical path: the copy of tile f+3 is in flight while
+//    tiles f..f+2 are transformed and gathered.
+//  * Producer thread p of group g (two groups of 4 warps, alternate tiles) holds
+//    128 values.  Round 1 reads its raw rows x = e + 2p + 256h (e = 0,1; h < 64)
+//    with LDS.64 (half-warps read 32 consecutive words: conflict-free), applies D,
+//    and runs the 7 butterfly stages over row bits {0, 8..13} in registers.  After a
+//    group barrier it writes the results into the "mid" layout
+//        mid(x) = col(x) + 130 row(x),  col = bits 1..7 of x,  row = bit 0 | bits 8..13 << 1
+//    (STS.32; a warp writes 32 consecutive words).  Round 2: thread p owns mid row p,
+//    reads it with LDS.64 (rows are 130 words apart, so a half-warp hits 16 distinct
+//    bank pairs), runs the stages over bits 1..7 and writes z = H_B D x back in place.
+//  * Consumer warps (8 x 32 threads, 64 accumulators each at r = 16384) gather
+//    z[k_lo] for their samples.  The packed 16-bit gather offsets live in tensor
+//    memory (TMEM, 32 KB) and are streamed per tile with tcgen05.ld, so they use no
+//    shared-memory bandwidth and no registers between tiles.  Tiles of a slab are
+//    visited in Gray-code order; the k_mid sign is carried as a frame (one
+//    conditional flip per visit, from a per-thread bit mask in shared memory).
+//
+// Hand-off: mbarrier FULL[b] (TMA complete, or tail tile released), named barriers
+// READY_b (z of buffer b written: 128 producer arrivals + 256 consumer syncs), GRP_g
+// (producer group), CONS (consumers; after it, consumer thread 0 refills buffer b).
+#include <cuda_runtime.h>
+
+#include "internal.cuh"
+
+namespace srht {
+namespace v3 {
+
+constexpr int LOG_B = 14;
+constexpr int B = 1 << LOG_B;
+constexpr int ROWW = 130;                  // mid-layout row stride in words
+constexpr int BUF_WORDS = 128 * ROWW;      // 16640 (raw tile needs 16384)
+constexpr int BUF_BYTES = BUF_WORDS * 4;   // 66560
+constexpr int NBUF = 3;
+constexpr int NCONS = 256;
+constexpr int NTHREADS = 512;
+constexpr int SIGN_OFF = NBUF * BUF_BYTES;            // per buffer: 128 threads x 16 B of D bits
+constexpr int MASK_OFF = SIGN_OFF + NBUF * 2048;
+constexpr int CTRL_OFF = MASK_OFF + V3_MAX_LOGJ * NCONS * 8;
+constexpr int SMEM_BYTES = CTRL_OFF + 256;  // 3 mbarriers, TMEM address, TmaState (<= 176 B)
+
+enum { BAR_READY0 = 1, BAR_GRP0 = 4, BAR_CONS = 6 };
+
+__host__ __device__ constexpr int mid(int x) { return ((x >> 1) & 127) + ROWW * ((x & 1) | ((x >> 8) << 1)); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ float flipf(float x, uint32_t mask) { return __uint_as_float(__float_as_uint(x) ^ mask); }
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra W_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Natural-order H_128 on 128 register values stored as 64 float2 (value u at v[u >> 1].x/.y).
+__device__ __forceinline__ void fwht128(float2 (&v)[64]) {
+#pragma unroll
+  for (int m = 0; m < 64; ++m) v[m] = __ffma2_rn(v[m], make_float2(1.f, -1.f), make_float2(v[m].y, v[m].x));
+#pragma unroll
+  for (int s = 1; s < 64; s <<= 1) {
+#pragma unroll
+    for (int m = 0; m < 64; ++m) {
+      if (!(m & s)) {
+        const float2 a = v[m], b = v[m | s];
+        v[m] = __fadd2_rn(a, b);
+        v[m | s] = __fadd2_rn(a, make_float2(-b.x, -b.y));
+      }
+    }
+  }
+}
+
+// Walk over the CTA's tiles: items blockIdx.x, +gridDim.x, ... (item = (column, slab));
+// inside an item, Gray-code steps pp = 0 .. np-1 visit tile j = gray(pp) when j < cnt.
+struct Cursor {
+  int it, pp, np, cnt, s, col;  // valid while it < n_items
+};
+
+__device__ __forceinline__ void cursor_item(const V3Params& P, Cursor& c) {
+  if (c.it >= P.n_items32) return;
+  c.col = c.it / P.S_act32;
+  c.s = c.it - c.col * P.S_act32;
+  const int rest = P.n_sub32 - c.s * P.J32;
+  c.cnt = rest < P.J32 ? rest : P.J32;
+  c.np = 1 << (32 - __clz(c.cnt - 1));  // next power of two >= cnt (cnt >= 1)
+  c.pp = 0;
+}
+__device__ __forceinline__ int gray(int pp) { return pp ^ (pp >> 1); }
+// Advance to the next ACTIVE tile (j < cnt).
+__device__ __forceinline__ void cursor_next_active(const V3Params& P, Cursor& c) {
+  while (c.it < P.n_items32) {
+    ++c.pp;
+    if (c.pp >= c.np) {
+      c.it += gridDim.x;
+      cursor_item(P, c);
+      if (c.it >= P.n_items32) return;
+    }
+    if (gray(c.pp) < c.cnt) return;
+  }
+}
+__device__ __forceinline__ void cursor_start(const V3Params& P, Cursor& c) {
+  c.it = blockIdx.x;
+  cursor_item(P, c);  // pp = 0: tile 0 is always active (cnt >= 1)
+}
+
+__device__ __forceinline__ const float* col_ptr(const V3Params& P, int col) {
+  const bool second = col >= P.ncols0;
+  const float* base = second ? P.src[1].vals : P.src[0].vals;
+  const int64_t ld = second ? P.src[1].ld : P.src[0].ld;
+  const int64_t lc = second ? col - P.ncols0 : col;
+  return base + lc * ld;
+}
+
+// Consumer thread 0 only: issue the copy of the next tile of the TMA cursor into buffer
+// f % 3 (its 64 KB of rows plus its 2 KB of packed D bits, one mbarrier transaction), and
+// an L2 prefetch of the tile NBUF further on.  The cursors live in shared memory, so they cost
+// the consumers no registers.
+struct TmaState {
+  Cursor cur, pf;
+  int f;  // flat index of the next tile to issue
+};
+static_assert(80 + sizeof(TmaState) <= 256, "control block overflows");
+
+__device__ __forceinline__ void tma_issue_next(const V3Params& P, TmaState& st, unsigned char* smem) {
+  const Cursor c = st.cur;
+  if (c.it >= P.n_items32) return;
+  const int f = st.f;
+  const int b = f % NBUF;
+  const uint32_t bar = smem_u32(smem + CTRL_OFF + 8 * b);
+  const int tile = c.s * P.J32 + gray(c.pp);
+  const int64_t row0 = (int64_t)tile * B;
+  const bool full = row0 + B <= P.n;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(full ? B * 4 + 2048 : 2048)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 2048, [%2];" ::"r"(
+                   smem_u32(smem + SIGN_OFF + 2048 * b)),
+               "l"(P.signs + ((int64_t)tile << 7)), "r"(bar)
+               : "memory");
+  if (full) {  // a tail tile is loaded by the producers themselves (guarded)
+    const char* src = reinterpret_cast<const char*>(col_ptr(P, c.col) + row0);
+    const uint32_t dst = smem_u32(smem + (size_t)b * BUF_BYTES);
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32768, [%2];" ::"r"(dst + k * 32768),
+          "l"(src + k * 32768), "r"(bar)
+          : "memory");
+  }
+  Cursor n = c;
+  cursor_next_active(P, n);
+  st.cur = n;
+  st.f = f + 1;
+  Cursor q = st.pf;
+  if (q.it < P.n_items32) {
+    const int64_t r0 = (int64_t)(q.s * P.J32 + gray(q.pp)) * B;
+    if (r0 + B <= P.n)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(col_ptr(P, q.col) + r0), "r"(B * 4) : "memory");
+    cursor_next_active(P, q);
+    st.pf = q;
+  }
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constant__ V3Params P) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint2* masks_s = reinterpret_cast<uint2*>(smem + MASK_OFF);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + 64);
+  TmaState& tma_st = *reinterpret_cast<TmaState*>(smem + CTRL_OFF + 80);
+  constexpr int MW = RPT / 2;                        // packed meta words (TMEM columns) per consumer thread
+  constexpr int TCOLS = (2 * MW) < 32 ? 32 : 2 * MW; // TMEM columns allocated (two consumer warps per lane quarter)
+  const int tid = threadIdx.x;
+
+  // ---------------- setup (all threads) ----------------
+  if (tid == 0) {
+    for (int b = 0; b < NBUF; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(smem + CTRL_OFF + 8 * b)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid >= 256 && tid < 288) {  // consumer warp 0 allocates TMEM
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid >= 256)
+    for (int i = tid - 256; i < P.log_j * NCONS; i += NCONS) masks_s[i] = P.masks[i];
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  if (tid < 256) {
+    // =========================== producers ===========================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
+    const int g = tid >> 7;
+    const int p = tid & 127;
+    const int n = (int)P.n;
+    Cursor cur;
+    cursor_start(P, cur);
+    int f = 0;
+    if (g == 1) {
+      cursor_next_active(P, cur);
+      f = 1;
+    }
+    while (cur.it < P.n_items32) {
+      const int b = f % NBUF;
+      const uint32_t parity = (uint32_t)((f / NBUF) & 1);
+      const int row0 = (cur.s * P.J32 + gray(cur.pp)) * B;
+      const float* __restrict__ colp = col_ptr(P, cur.col);
+      float* buf = reinterpret_cast<float*>(smem + (size_t)b * BUF_BYTES);
+      mbar_wait(smem_u32(smem + CTRL_OFF + 8 * b), parity);
+      const uint4 sg = *reinterpret_cast<const uint4*>(smem + SIGN_OFF + 2048 * b + 16 * p);
+      float2 v[64];
+      // ---- round 1: rows x = e + 2p + 256h ----
+      if (row0 + B <= n) {
+#pragma unroll
+        for (int h = 0; h < 64; ++h) v[h] = *reinterpret_cast<const float2*>(buf + 2 * p + 256 * h);
+      } else {
+#pragma unroll
+        for (int h = 0; h < 64; ++h) {
+          const int row = row0 + 2 * p + 256 * h;
+          v[h] = make_float2(row < n ? colp[row] : 0.f, row + 1 < n ? colp[row + 1] : 0.f);
+        }
+      }
+      // D: sign of (h, e) = bit 2(h & 15) + e of word h >> 4
+#pragma unroll
+      for (int h = 0; h < 64; ++h) {
+        const uint32_t w = (h >> 4) == 0 ? sg.x : (h >> 4) == 1 ? sg.y : (h >> 4) == 2 ? sg.z : sg.w;
+        const int bt = (h & 15) << 1;
+        // funnel shifts keep the bit moves on the ALU pipe (IMAD.SHL would take FMA slots)
+        v[h].x = flipf(v[h].x, __funnelshift_l(w, w, 31 - bt) & 0x80000000u);
+        v[h].y = flipf(v[h].y, __funnelshift_l(w, w, 30 - bt) & 0x80000000u);
+      }
+      fwht128(v);  // row bits 0 (pair) and 8..13 (h)
+      bar_sync(BAR_GRP0 + g, 128);  // every raw row of the tile is in registers
+#pragma unroll
+      for (int h = 0; h < 64; ++h) {
+        buf[p + ROWW * (2 * h)] = v[h].x;      // mid(x): col = p, row = 2h + e
+        buf[p + ROWW * (2 * h + 1)] = v[h].y;
+      }
+      bar_sync(BAR_GRP0 + g, 128);
+      // ---- round 2: mid row p, cols 2m + e ----
+      float* rowp = buf + ROWW * p;
+#pragma unroll
+      for (int m = 0; m < 64; ++m) v[m] = *reinterpret_cast<const float2*>(rowp + 2 * m);
+      fwht128(v);  // row bits 1 (pair) and 2..7 (m)
+#pragma unroll
+      for (int m = 0; m < 64; ++m) *reinterpret_cast<float2*>(rowp + 2 * m) = v[m];
+      bar_arrive(BAR_READY0 + b, 384);
+      // next tile of this group: two active tiles ahead
+      cursor_next_active(P, cur);
+      cursor_next_active(P, cur);
+      f += 2;
+    }
+  } else {
+    // =========================== consumers ===========================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+    const int c = tid - 256;
+    const int wc = c >> 5;
+    const uint32_t tbase = *tmem_slot;
+    const uint32_t taddr = tbase + ((uint32_t)(32 * (wc & 3)) << 16) + (uint32_t)((wc >> 2) * MW);
+    // meta -> TMEM (once)
+#pragma unroll
+    for (int k = 0; k < MW; k += 4) {
+      const uint4 m4 = __ldg(reinterpret_cast<const uint4*>(P.meta + (size_t)c * MW + k));
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + k), "r"(m4.x),
+                   "r"(m4.y), "r"(m4.z), "r"(m4.w)
+                   : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    if (c == 0) {  // tiles 0..2 into the ring
+      Cursor c0;
+      cursor_start(P, c0);
+      tma_st.cur = c0;
+      tma_st.f = 0;
+      for (int k = 0; k < NBUF; ++k) cursor_next_active(P, c0);
+      tma_st.pf = c0;  // issuing tile t prefetches tile t + NBUF into L2
+      for (int k = 0; k < NBUF; ++k) tma_issue_next(P, tma_st, smem);
+    }
+    float acc[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) acc[q] = 0.f;
+    int f = 0;
+    for (int it = blockIdx.x; it < P.n_items32; it += gridDim.x) {
+      Cursor ci;
+      ci.it = it;
+      cursor_item(P, ci);
+      const int col = ci.col, s = ci.s, cnt = ci.cnt, np = ci.np;
+      for (int pp = 0; pp < np; ++pp) {
+        uint2 mk = make_uint2(0u, 0u);
+        if (pp) mk = masks_s[(__ffs(pp) - 1) * NCONS + c];
+        if (gray(pp) < cnt) {
+          const int b = f % NBUF;
+          const float* buf = reinterpret_cast<const float*>(smem + (size_t)b * BUF_BYTES);
+          bar_sync(BAR_READY0 + b, 384);
+          constexpr int CH = MW < 8 ? MW : 8;  // meta words per TMEM load
+#pragma unroll
+          for (int k = 0; k < MW; k += CH) {
+            uint32_t w[CH];
+            if constexpr (CH == 8) {
+              asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                           : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                             "=r"(w[7])
+                           : "r"(taddr + k));
+            } else {
+              asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                           : "r"(taddr + k));
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 2 * CH; ++i) {
+              const int q = 2 * k + i;
+              // word = lo | hi << 17 (15-bit word offsets; bits 15, 16 clear), so the high
+              // sample's byte offset is w >> 15
+              const float z = (i & 1) ? *reinterpret_cast<const float*>(reinterpret_cast<const char*>(buf) + (w[i >> 1] >> 15))
+                                      : buf[w[i >> 1] & 0x7fffu];
+              const uint32_t mw = q < 32 ? mk.x : mk.y;
+              acc[q] = flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u) + z;
+            }
+          }
+          bar_sync(BAR_CONS, NCONS);  // every consumer is done with buffer b
+          if (c == 0) tma_issue_next(P, tma_st, smem);
+          ++f;
+        } else {
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const uint32_t mw = q < 32 ? mk.x : mk.y;
+            acc[q] = flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u);
+          }
+        }
+      }
+      // ---- slab epilogue: undo the frame sign of the last step, write ----
+      const uint32_t jlast = (uint32_t)gray(np - 1);
+      const bool second = col >= P.ncols0;
+      float* __restrict__ outp = second ? P.src[1].out : P.src[0].out;
+      const int64_t ldo = second ? P.src[1].ldo : P.src[0].ldo;
+      const int64_t lc = second ? col - P.ncols0 : col;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int pk = P.perm[q * NCONS + c];
+        if (pk >= 0) {
+          const int t = pk & 0xffff;
+          const uint32_t kmid = (uint32_t)pk >> 16;
+          const float a = flipf(acc[q], (uint32_t)(__popc(kmid & jlast) & 1) << 31);
+          if (P.S_act == 1) outp[lc * ldo + t] = a * P.scale;
+          else P.partials[((int64_t)s * P.total_cols + col) * P.r + t] = a;
+        }
+        acc[q] = 0.f;
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    bar_sync(BAR_CONS, NCONS);
+    if (wc == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(TCOLS));
+    }
+  }
+}
+
+template <int RPT>
+cudaError_t launch_rpt(const V3Params& vp, int grid, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_sketch_tma<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_sketch_tma<RPT><<<grid, NTHREADS, SMEM_BYTES, stream>>>(vp);
+  return cudaGetLastError();
+}
+
+}  // namespace v3
+
+int v3_mid(int x) { return v3::mid(x); }
+
+cudaError_t launch_sketch_tma(const srht_plan* P, const V3Params& vp, cudaStream_t stream) {
+  if (vp.total_cols <= 0) return cudaSuccess;
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = vp.n_items32 < sms ? vp.n_items32 : sms;
+  switch (P->rpt2) {
+    case 8: return v3::launch_rpt<8>(vp, grid, stream);
+    case 16: return v3::launch_rpt<16>(vp, grid, stream);
+    case 32: return v3::launch_rpt<32>(vp, grid, stream);
+    case 64: return v3::launch_rpt<64>(vp, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace srht
