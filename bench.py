@@ -81,7 +81,7 @@ def load_traffic(config, kernel):
         return None
 
 
-KERNEL_NAMES = {1: "k_sketch_tiles", 2: "k_sketch_ws", 3: "k_sketch_tma"}
+KERNEL_NAMES = {1: "k_sketch_tiles", 2: "k_sketch_ws", 3: "k_sketch_tma", 4: "k_sketch_f64"}
 
 
 def last_kernel(lib):

@@ -91,6 +91,25 @@ srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r,
                                      uint64_t seed, int64_t batch,
                                      srht_plan** out);
 
+/* Plan flags for srht_plan_create_ex. */
+enum {
+  /* Every sketch of this plan accumulates in FP64: FP32 inputs are widened,
+   * the Hadamard butterflies, the pruned accumulation and the slab sums run
+   * in FP64, and each output is rounded once to FP32 (close to the correctly
+   * rounded FP32 sketch).  This is the parity mode of DESIGN.md reading R14
+   * (the 1e-6 end-to-end NNLS gate of BASELINE.json's north_star sits at the
+   * FP32 rounding floor); it is several times slower than the
+   * default FP32 path, which it does not replace.  Workspace: FP64 partials
+   * (srht_workspace_bytes accounts for it).                                  */
+  SRHT_PLAN_ACCUM_FP64 = 1
+};
+
+/* srht_plan_create_batched with flags (0 or SRHT_PLAN_ACCUM_FP64); any other
+ * bit is SRHT_EINVAL.  Same requirements and errors otherwise.               */
+srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed,
+                                int64_t batch, uint32_t flags,
+                                srht_plan** out);
+
 srht_status srht_plan_destroy(srht_plan* plan); /* NULL is a no-op */
 
 /* N (padded size), r and batch of a plan; any output pointer may be NULL.    */

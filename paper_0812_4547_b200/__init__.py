@@ -102,11 +102,15 @@ class Plan:
     Philox streams (R4); problem p uses streams (seed, 2p), (seed, 2p+1).
     """
 
-    def __init__(self, n, d, r, seed=0, batch=1):
+    def __init__(self, n, d, r, seed=0, batch=1, accum="fp32"):
+        if accum not in ("fp32", "fp64"):
+            raise ValueError("accum must be 'fp32' or 'fp64'")
         self._lib = _lib.load()
         self._h = ctypes.c_void_p()
-        check(self._lib.srht_plan_create_batched(int(n), int(d), int(r), ctypes.c_uint64(int(seed) & (2**64 - 1)),
-                                                 int(batch), ctypes.byref(self._h)), "srht_plan_create_batched")
+        flags = _lib.SRHT_PLAN_ACCUM_FP64 if accum == "fp64" else 0
+        check(self._lib.srht_plan_create_ex(int(n), int(d), int(r), ctypes.c_uint64(int(seed) & (2**64 - 1)),
+                                            int(batch), flags, ctypes.byref(self._h)), "srht_plan_create_ex")
+        self.accum = accum
         N, rr, bb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         check(self._lib.srht_plan_info(self._h, ctypes.byref(N), ctypes.byref(rr), ctypes.byref(bb)), "srht_plan_info")
         self.n, self.d, self.r, self.N, self.batch, self.seed = int(n), int(d), int(rr.value), int(N.value), int(bb.value), int(seed)

@@ -9,6 +9,8 @@ LIB_PATH = os.path.join(_HERE, os.environ.get("SRHT_LIB", "libsrht.so"))
 SRHT_DENSE = 0
 SRHT_CSC = 1
 
+SRHT_PLAN_ACCUM_FP64 = 1
+
 SRHT_OK = 0
 SRHT_EINVAL = 1
 SRHT_ENOMEM = 2
@@ -38,6 +40,7 @@ _MP = ctypes.POINTER(SrhtMatrix)
 SIGNATURES = [
     ("srht_plan_create", ctypes.c_int, [_I64, _I64, _I64, _U64, _PP]),
     ("srht_plan_create_batched", ctypes.c_int, [_I64, _I64, _I64, _U64, _I64, _PP]),
+    ("srht_plan_create_ex", ctypes.c_int, [_I64, _I64, _I64, _U64, _I64, ctypes.c_uint32, _PP]),
     ("srht_plan_destroy", ctypes.c_int, [_P]),
     ("srht_plan_info", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("srht_plan_copy_indices", ctypes.c_int, [_P, _I64, _P]),

@@ -51,6 +51,11 @@ srht::ColSrc make_src(const srht_matrix* M, float* out, int64_t ldo) {
 
 size_t partial_bytes(const srht_plan* P, int64_t ncols) {
   if (ncols <= 0) return 0;
+  if (P->flags & SRHT_PLAN_ACCUM_FP64) {  // FP64 partials of the v1 slab geometry
+    if (P->S_act <= 1) return 0;
+    const size_t b = (size_t)P->S_act * (size_t)ncols * (size_t)P->r * sizeof(double);
+    return (b + 255) & ~size_t(255);
+  }
   int64_t S = P->S_act > 1 ? P->S_act : 0;
   if (P->ws_ok && P->S_act2 > 1 && P->S_act2 > S) S = P->S_act2;
   if (S <= 1) return 0;
@@ -172,6 +177,11 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
   if (cudaGetDevice(&dev) != cudaSuccess) return SRHT_ECUDA;
   if (dev != P->device) return SRHT_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (P->flags & SRHT_PLAN_ACCUM_FP64) {
+    sp.partials64 = static_cast<double*>(ws);
+    sp.partials = nullptr;
+    return srht::launch_sketch_f64(P, sp, st) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+  }
   const bool batched = sp.cols_per_problem != INT64_MAX;
   if (P->ws_ok && !batched) {
     // dense sources -> kernel v2; CSC sources -> kernel v1 (separate launches)
@@ -218,6 +228,7 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       vp.n_sub32 = (int)vp.n_sub;
       vp.scale = P->scale;
       vp.partials = sp.partials;
+      vp.trace = srht::g_debug_trace;
       const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
       if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
       cudaError_t e = srht::launch_sketch_tma(P, vp, st);
@@ -304,11 +315,12 @@ const char* srht_status_str(srht_status s) {
   return "unknown srht_status";
 }
 
-srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t seed, int64_t batch,
-                                     srht_plan** out) {
+srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, int64_t batch, uint32_t flags,
+                                srht_plan** out) {
   if (!out) return SRHT_EINVAL;
   *out = nullptr;
   if (n < 1 || d < 0 || r < 1 || batch < 1 || batch > 65535) return SRHT_EINVAL;
+  if (flags & ~(uint32_t)SRHT_PLAN_ACCUM_FP64) return SRHT_EINVAL;
   int64_t N = 2;
   while (N < n) N *= 2;
   if (r > N) return SRHT_EINVAL;
@@ -323,6 +335,7 @@ srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t s
   P->N = N;
   P->batch = batch;
   P->seed = seed;
+  P->flags = flags;
   // Geometry (depends on n and r only).  Tile B ~ r (so ~1 sampled entry per
   // tile row, Ailon-Liberty balance), clamped to [2^10, 2^14]; slabs of ~2^20 rows.
   int lb = ceil_log2(r);
@@ -370,7 +383,8 @@ srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t s
   cudaError_t e = srht::build_plan_device(P, st);
   cudaStreamDestroy(st);
   // Kernel v2 geometry (dense single problems): B = 2^14, slabs of 2^20 rows.
-  if (e == cudaSuccess && batch == 1 && N >= (int64_t(1) << 14) && r <= 16384) {
+  // (Not built for FP64-accumulation plans, which always run the FP64 kernel.)
+  if (e == cudaSuccess && !(flags & SRHT_PLAN_ACCUM_FP64) && batch == 1 && N >= (int64_t(1) << 14) && r <= 16384) {
     P->ws_ok = true;
     // Slab = J2 tiles; J2 ~ 64 r / 2^14 keeps the slab partials (r floats per
     // slab) near 3% of the input, and slabs small enough to load-balance.
@@ -409,8 +423,13 @@ srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t s
   return SRHT_OK;
 }
 
+srht_status srht_plan_create_batched(int64_t n, int64_t d, int64_t r, uint64_t seed, int64_t batch,
+                                     srht_plan** out) {
+  return srht_plan_create_ex(n, d, r, seed, batch, 0u, out);
+}
+
 srht_status srht_plan_create(int64_t n, int64_t d, int64_t r, uint64_t seed, srht_plan** out) {
-  return srht_plan_create_batched(n, d, r, seed, 1, out);
+  return srht_plan_create_ex(n, d, r, seed, 1, 0u, out);
 }
 
 srht_status srht_plan_destroy(srht_plan* P) {

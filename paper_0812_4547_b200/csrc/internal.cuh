@@ -8,6 +8,7 @@
 struct srht_plan {
   int64_t n, d, r, N, batch;
   uint64_t seed;
+  uint32_t flags;   // SRHT_PLAN_ACCUM_FP64: every sketch runs the FP64-accumulation kernel
   // Tile / slab geometry: depends on (n, r) only.
   int log_b;        // tile bits; B = 2^log_b rows per sub-block
   int64_t B;
@@ -78,7 +79,10 @@ struct SketchParams {
   float scale;
   double scale_f64;           // r^{-1/2} in FP64 (slab reduction)
   float* partials;            // [S_act][total_cols][r] when S_act > 1
+  double* partials64;         // FP64 mode: [S_act][total_cols][r] when S_act > 1
 };
+// FP64-accumulation parity mode (sketch_f64.cu), v1 slab geometry.
+cudaError_t launch_sketch_f64(const srht_plan* P, const SketchParams& sp, cudaStream_t stream);
 
 cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream_t stream);
 
@@ -117,6 +121,7 @@ struct V3Params {
   int n_items32, S_act32, J32, n_sub32;  // the same, 32-bit (checked on the host)
   float scale;
   float* partials;        // [S_act][total_cols][r] when S_act > 1
+  unsigned long long* trace;  // experiment phase timestamps (srht_debug_set_trace), else null
 };
 cudaError_t launch_sketch_tma(const srht_plan* P, const V3Params& vp, cudaStream_t stream);
 int v3_mid(int x);  // kernel-v3 z layout (host side, for the slot layout)

@@ -47,9 +47,9 @@ constexpr int NTHREADS = 512;
 constexpr int SIGN_OFF = NBUF * BUF_BYTES;            // per buffer: 128 threads x 16 B of D bits
 constexpr int MASK_OFF = SIGN_OFF + NBUF * 2048;
 constexpr int CTRL_OFF = MASK_OFF + V3_MAX_LOGJ * NCONS * 8;
-constexpr int SMEM_BYTES = CTRL_OFF + 256;  // 3 mbarriers, TMEM address, TmaState (<= 176 B)
+constexpr int SMEM_BYTES = CTRL_OFF + 256;  // mbarriers [0,24), TMEM address [32,36), slot states [64,..)
 
-enum { BAR_READY0 = 1, BAR_GRP0 = 4, BAR_CONS = 6 };
+enum { BAR_READY0 = 1, BAR_GRP0 = 4, BAR_CONS = 6 };  // named barriers (0 = __syncthreads)
 
 __host__ __device__ constexpr int mid(int x) { return ((x >> 1) & 127) + ROWW * ((x & 1) | ((x >> 8) << 1)); }
 
@@ -59,6 +59,19 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ float flipf(float x, uint32_t mask) { return __uint_as_float(__float_as_uint(x) ^ mask); }
+
+template <int CH>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&w)[CH]) {
+  if constexpr (CH == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "r"(taddr));
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "r"(taddr));
+  }
+}
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -82,6 +95,32 @@ __device__ __forceinline__ void fwht128(float2 (&v)[64]) {
       }
     }
   }
+}
+
+// The same transform split for software pipelining inside one warp: the pair stage and
+// the stages over m-bits 0..3 touch only the 16 float2 of quarter q (m in [16q, 16q+16)),
+// so they can run as soon as that quarter's loads land; stage_m(S) is one cross stage.
+__device__ __forceinline__ void fwht_quarter(float2 (&v)[64], int q) {
+#pragma unroll
+  for (int m = 16 * q; m < 16 * q + 16; ++m)
+    v[m] = __ffma2_rn(v[m], make_float2(1.f, -1.f), make_float2(v[m].y, v[m].x));
+#pragma unroll
+  for (int s = 1; s < 16; s <<= 1) {
+#pragma unroll
+    for (int m = 16 * q; m < 16 * q + 16; ++m) {
+      if (!(m & s)) {
+        const float2 a = v[m], b = v[m | s];
+        v[m] = __fadd2_rn(a, b);
+        v[m | s] = __fadd2_rn(a, make_float2(-b.x, -b.y));
+      }
+    }
+  }
+}
+template <int S>
+__device__ __forceinline__ void bfly(float2 (&v)[64], int m) {
+  const float2 a = v[m], b = v[m | S];
+  v[m] = __fadd2_rn(a, b);
+  v[m | S] = __fadd2_rn(a, make_float2(-b.x, -b.y));
 }
 
 // Walk over the CTA's tiles: items blockIdx.x, +gridDim.x, ... (item = (column, slab));
@@ -125,25 +164,33 @@ __device__ __forceinline__ const float* col_ptr(const V3Params& P, int col) {
   return base + lc * ld;
 }
 
-// Consumer thread 0 only: issue the copy of the next tile of the TMA cursor into buffer
-// f % 3 (its 64 KB of rows plus its 2 KB of packed D bits, one mbarrier transaction), and
-// an L2 prefetch of the tile NBUF further on.  The cursors live in shared memory, so they cost
-// the consumers no registers.
-struct TmaState {
-  Cursor cur, pf;
-  int f;  // flat index of the next tile to issue
+// TMA issue.  Buffer slot b (tiles f = b, b+3, ...) keeps its own cursor: the next tile to
+// load into it.  The consumer warp that finishes tile f last (shared-memory counter per
+// slot) refills the slot: tile f+3's 64 KB of rows plus its 2 KB of packed D bits, one
+// mbarrier transaction; then it advances the slot cursor by three active tiles and
+// prefetches that tile (f+6) into L2.  No consumer waits for another, and the cursors
+// cost the consumers no registers.
+struct SlotState {
+  Cursor cur;   // next tile for this slot
+  int count;    // consumer warps done with the slot's current tile
 };
-static_assert(80 + sizeof(TmaState) <= 256, "control block overflows");
+static_assert(64 + NBUF * sizeof(SlotState) <= 256, "control block overflows");
 
-__device__ __forceinline__ void tma_issue_next(const V3Params& P, TmaState& st, unsigned char* smem) {
-  const Cursor c = st.cur;
-  if (c.it >= P.n_items32) return;
-  const int f = st.f;
-  const int b = f % NBUF;
-  const uint32_t bar = smem_u32(smem + CTRL_OFF + 8 * b);
-  const int tile = c.s * P.J32 + gray(c.pp);
+__device__ __forceinline__ void tile_src(const V3Params& P, const Cursor& c, int& tile, const float*& src, bool& full) {
+  tile = c.s * P.J32 + gray(c.pp);
   const int64_t row0 = (int64_t)tile * B;
-  const bool full = row0 + B <= P.n;
+  full = row0 + B <= P.n;
+  src = col_ptr(P, c.col) + row0;
+}
+
+__device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int b, unsigned char* smem) {
+  Cursor c = st.cur;
+  if (c.it >= P.n_items32) return;
+  const uint32_t bar = smem_u32(smem + CTRL_OFF + 8 * b);
+  int tile;
+  const float* src;
+  bool full;
+  tile_src(P, c, tile, src, full);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(full ? B * 4 + 2048 : 2048)
                : "memory");
@@ -152,35 +199,35 @@ __device__ __forceinline__ void tma_issue_next(const V3Params& P, TmaState& st, 
                "l"(P.signs + ((int64_t)tile << 7)), "r"(bar)
                : "memory");
   if (full) {  // a tail tile is loaded by the producers themselves (guarded)
-    const char* src = reinterpret_cast<const char*>(col_ptr(P, c.col) + row0);
     const uint32_t dst = smem_u32(smem + (size_t)b * BUF_BYTES);
 #pragma unroll
     for (int k = 0; k < 2; ++k)
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32768, [%2];" ::"r"(dst + k * 32768),
-          "l"(src + k * 32768), "r"(bar)
+          "l"(reinterpret_cast<const char*>(src) + k * 32768), "r"(bar)
           : "memory");
   }
-  Cursor n = c;
-  cursor_next_active(P, n);
-  st.cur = n;
-  st.f = f + 1;
-  Cursor q = st.pf;
-  if (q.it < P.n_items32) {
-    const int64_t r0 = (int64_t)(q.s * P.J32 + gray(q.pp)) * B;
-    if (r0 + B <= P.n)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(col_ptr(P, q.col) + r0), "r"(B * 4) : "memory");
-    cursor_next_active(P, q);
-    st.pf = q;
+#pragma unroll
+  for (int k = 0; k < NBUF; ++k) cursor_next_active(P, c);
+  st.cur = c;
+  if (c.it < P.n_items32) {
+    tile_src(P, c, tile, src, full);
+    if (full) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(B * 4) : "memory");
   }
 }
 
-template <int RPT>
+// Experiment tracing (TR = true only when srht_debug_set_trace gave a buffer): clock64 at
+// phase boundaries of CTA 0, for flat tiles 16..79; see scripts/v3_trace.py.
+#define V3_TRACE(role, k, pt)                                                            \
+  if (TR && blockIdx.x == 0 && (k) >= 16 && (k) < 80)                                    \
+    P.trace[((size_t)(role) * 64 + ((k) - 16)) * 8 + (pt)] = clock64();
+
+template <int RPT, bool TR>
 __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constant__ V3Params P) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint2* masks_s = reinterpret_cast<uint2*>(smem + MASK_OFF);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + 64);
-  TmaState& tma_st = *reinterpret_cast<TmaState*>(smem + CTRL_OFF + 80);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + 32);
+  SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + 64);
   constexpr int MW = RPT / 2;                        // packed meta words (TMEM columns) per consumer thread
   constexpr int TCOLS = (2 * MW) < 32 ? 32 : 2 * MW; // TMEM columns allocated (two consumer warps per lane quarter)
   const int tid = threadIdx.x;
@@ -221,45 +268,75 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       const int row0 = (cur.s * P.J32 + gray(cur.pp)) * B;
       const float* __restrict__ colp = col_ptr(P, cur.col);
       float* buf = reinterpret_cast<float*>(smem + (size_t)b * BUF_BYTES);
+      if (p == 0) { V3_TRACE(g, f, 0) }
       mbar_wait(smem_u32(smem + CTRL_OFF + 8 * b), parity);
+      if (p == 0) { V3_TRACE(g, f, 6) }
       const uint4 sg = *reinterpret_cast<const uint4*>(smem + SIGN_OFF + 2048 * b + 16 * p);
       float2 v[64];
-      // ---- round 1: rows x = e + 2p + 256h ----
-      if (row0 + B <= n) {
-#pragma unroll
-        for (int h = 0; h < 64; ++h) v[h] = *reinterpret_cast<const float2*>(buf + 2 * p + 256 * h);
-      } else {
-#pragma unroll
+      // ---- round 1: rows x = e + 2p + 256h; quarter q = h in [16q, 16q+16) ----
+      if (row0 + B > n) {
+        // tail tile (not copied by TMA): the group stages it in the raw layout itself,
+        // zero-filling rows >= n, then reads it back like any other tile
+#pragma unroll 4
         for (int h = 0; h < 64; ++h) {
           const int row = row0 + 2 * p + 256 * h;
-          v[h] = make_float2(row < n ? colp[row] : 0.f, row + 1 < n ? colp[row + 1] : 0.f);
+          *reinterpret_cast<float2*>(buf + 2 * p + 256 * h) =
+              make_float2(row < n ? colp[row] : 0.f, row + 1 < n ? colp[row + 1] : 0.f);
         }
+        bar_sync(BAR_GRP0 + g, 128);
       }
-      // D: sign of (h, e) = bit 2(h & 15) + e of word h >> 4
 #pragma unroll
-      for (int h = 0; h < 64; ++h) {
-        const uint32_t w = (h >> 4) == 0 ? sg.x : (h >> 4) == 1 ? sg.y : (h >> 4) == 2 ? sg.z : sg.w;
-        const int bt = (h & 15) << 1;
-        // funnel shifts keep the bit moves on the ALU pipe (IMAD.SHL would take FMA slots)
-        v[h].x = flipf(v[h].x, __funnelshift_l(w, w, 31 - bt) & 0x80000000u);
-        v[h].y = flipf(v[h].y, __funnelshift_l(w, w, 30 - bt) & 0x80000000u);
-      }
-      fwht128(v);  // row bits 0 (pair) and 8..13 (h)
-      bar_sync(BAR_GRP0 + g, 128);  // every raw row of the tile is in registers
+      for (int q = 0; q < 4; ++q) {
 #pragma unroll
-      for (int h = 0; h < 64; ++h) {
-        buf[p + ROWW * (2 * h)] = v[h].x;      // mid(x): col = p, row = 2h + e
-        buf[p + ROWW * (2 * h + 1)] = v[h].y;
+        for (int h = 16 * q; h < 16 * q + 16; ++h) v[h] = *reinterpret_cast<const float2*>(buf + 2 * p + 256 * h);
+        // D: sign of (h, e) = bit 2(h & 15) + e of word h >> 4 (= word q).  Funnel shifts
+        // keep the bit moves on the ALU pipe (IMAD.SHL would take FMA slots).
+        const uint32_t w = q == 0 ? sg.x : q == 1 ? sg.y : q == 2 ? sg.z : sg.w;
+#pragma unroll
+        for (int h = 16 * q; h < 16 * q + 16; ++h) {
+          const int bt = (h & 15) << 1;
+          v[h].x = flipf(v[h].x, __funnelshift_l(w, w, 31 - bt) & 0x80000000u);
+          v[h].y = flipf(v[h].y, __funnelshift_l(w, w, 30 - bt) & 0x80000000u);
+        }
+        fwht_quarter(v, q);  // row bit 0 (pair) and bits 8..11 (h bits 0..3)
       }
+      if (p == 0) { V3_TRACE(g, f, 1) }
+#pragma unroll
+      for (int m = 0; m < 64; ++m)
+        if (!(m & 16)) bfly<16>(v, m);  // row bit 12
+      if (p == 0) { V3_TRACE(g, f, 2) }
+      bar_sync(BAR_GRP0 + g, 128);  // every raw row of the tile has been read
+      // row bit 13, each result stored as soon as it is final: mid(x) = p + 130 (2h + e)
+#pragma unroll
+      for (int m = 0; m < 32; ++m) {
+        bfly<32>(v, m);
+        buf[p + ROWW * (2 * m)] = v[m].x;
+        buf[p + ROWW * (2 * m + 1)] = v[m].y;
+        buf[p + ROWW * (2 * (m + 32))] = v[m + 32].x;
+        buf[p + ROWW * (2 * (m + 32) + 1)] = v[m + 32].y;
+      }
+      if (p == 0) { V3_TRACE(g, f, 3) }
       bar_sync(BAR_GRP0 + g, 128);
-      // ---- round 2: mid row p, cols 2m + e ----
+      // ---- round 2: mid row p, cols 2m + e; quarter-ordered like round 1 ----
       float* rowp = buf + ROWW * p;
 #pragma unroll
-      for (int m = 0; m < 64; ++m) v[m] = *reinterpret_cast<const float2*>(rowp + 2 * m);
-      fwht128(v);  // row bits 1 (pair) and 2..7 (m)
+      for (int q = 0; q < 4; ++q) {
 #pragma unroll
-      for (int m = 0; m < 64; ++m) *reinterpret_cast<float2*>(rowp + 2 * m) = v[m];
+        for (int m = 16 * q; m < 16 * q + 16; ++m) v[m] = *reinterpret_cast<const float2*>(rowp + 2 * m);
+        fwht_quarter(v, q);  // row bit 1 (pair) and bits 2..5 (m bits 0..3)
+      }
+#pragma unroll
+      for (int m = 0; m < 64; ++m)
+        if (!(m & 16)) bfly<16>(v, m);  // row bit 6
+      if (p == 0) { V3_TRACE(g, f, 4) }
+#pragma unroll
+      for (int m = 0; m < 32; ++m) {  // row bit 7, then z = H_B D x stored in place
+        bfly<32>(v, m);
+        *reinterpret_cast<float2*>(rowp + 2 * m) = v[m];
+        *reinterpret_cast<float2*>(rowp + 2 * (m + 32)) = v[m + 32];
+      }
       bar_arrive(BAR_READY0 + b, 384);
+      if (p == 0) { V3_TRACE(g, f, 5) }
       // next tile of this group: two active tiles ahead
       cursor_next_active(P, cur);
       cursor_next_active(P, cur);
@@ -281,14 +358,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
                    : "memory");
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    if (c == 0) {  // tiles 0..2 into the ring
+    if (c == 0) {  // slot b starts at active tile b; fill the ring, prefetch tiles 3..5
       Cursor c0;
       cursor_start(P, c0);
-      tma_st.cur = c0;
-      tma_st.f = 0;
-      for (int k = 0; k < NBUF; ++k) cursor_next_active(P, c0);
-      tma_st.pf = c0;  // issuing tile t prefetches tile t + NBUF into L2
-      for (int k = 0; k < NBUF; ++k) tma_issue_next(P, tma_st, smem);
+      for (int b = 0; b < NBUF; ++b) {
+        slots[b].cur = c0;
+        slots[b].count = 0;
+        cursor_next_active(P, c0);
+      }
+      for (int b = 0; b < NBUF; ++b) tma_issue(P, slots[b], b, smem);
     }
     float acc[RPT];
 #pragma unroll
@@ -305,35 +383,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
         if (gray(pp) < cnt) {
           const int b = f % NBUF;
           const float* buf = reinterpret_cast<const float*>(smem + (size_t)b * BUF_BYTES);
+          if (c == 0) { V3_TRACE(2, f, 0) }
           bar_sync(BAR_READY0 + b, 384);
           constexpr int CH = MW < 8 ? MW : 8;  // meta words per TMEM load
+          uint32_t w[2][CH];
+          tmem_ld<CH>(taddr, w[0]);
 #pragma unroll
           for (int k = 0; k < MW; k += CH) {
-            uint32_t w[CH];
-            if constexpr (CH == 8) {
-              asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                           : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
-                             "=r"(w[7])
-                           : "r"(taddr + k));
-            } else {
-              asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                           : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
-                           : "r"(taddr + k));
-            }
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (k + CH < MW) tmem_ld<CH>(taddr + k + CH, w[((k / CH) + 1) & 1]);  // next chunk in flight
+            if (k == 0 && c == 0) { V3_TRACE(2, f, 1) }
+            const uint32_t* wk = w[(k / CH) & 1];
 #pragma unroll
             for (int i = 0; i < 2 * CH; ++i) {
               const int q = 2 * k + i;
               // word = lo | hi << 17 (15-bit word offsets; bits 15, 16 clear), so the high
               // sample's byte offset is w >> 15
-              const float z = (i & 1) ? *reinterpret_cast<const float*>(reinterpret_cast<const char*>(buf) + (w[i >> 1] >> 15))
-                                      : buf[w[i >> 1] & 0x7fffu];
+              const float z = (i & 1) ? *reinterpret_cast<const float*>(reinterpret_cast<const char*>(buf) + (wk[i >> 1] >> 15))
+                                      : buf[wk[i >> 1] & 0x7fffu];
               const uint32_t mw = q < 32 ? mk.x : mk.y;
               acc[q] = flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u) + z;
             }
           }
-          bar_sync(BAR_CONS, NCONS);  // every consumer is done with buffer b
-          if (c == 0) tma_issue_next(P, tma_st, smem);
+          if (c == 0) { V3_TRACE(2, f, 2) }
+          // the last consumer warp done with buffer b refills it (no consumer-wide barrier)
+          __syncwarp();
+          if ((c & 31) == 0) {
+            const int done = atomicAdd(&slots[b].count, 1);
+            if (done == NCONS / 32 - 1) {
+              slots[b].count = 0;
+              tma_issue(P, slots[b], b, smem);
+            }
+          }
+          if (c == 0) { V3_TRACE(2, f, 3) }
           ++f;
         } else {
 #pragma unroll
@@ -371,17 +453,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
   }
 }
 
-template <int RPT>
-cudaError_t launch_rpt(const V3Params& vp, int grid, cudaStream_t stream) {
+template <int RPT, bool TR>
+cudaError_t launch_tr(const V3Params& vp, int grid, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
     const cudaError_t e =
-        cudaFuncSetAttribute(k_sketch_tma<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_sketch_tma<RPT, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_sketch_tma<RPT><<<grid, NTHREADS, SMEM_BYTES, stream>>>(vp);
+  k_sketch_tma<RPT, TR><<<grid, NTHREADS, SMEM_BYTES, stream>>>(vp);
   return cudaGetLastError();
+}
+template <int RPT>
+cudaError_t launch_rpt(const V3Params& vp, int grid, cudaStream_t stream) {
+  return vp.trace ? launch_tr<RPT, true>(vp, grid, stream) : launch_tr<RPT, false>(vp, grid, stream);
 }
 
 }  // namespace v3

@@ -1,0 +1,45 @@
+"""Per-phase timing of kernel v3 on CTA 0 (clock64 at phase boundaries; experiment only).
+
+python scripts/v3_trace.py [n d r]  (default: config-4 shape 2^20 x 513, r = 8192)
+Group g producer warp 0 (tiles f = g, g+2, ...) and consumer thread 0, flat tiles 16..79."""
+import ctypes
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, '.')
+import paper_0812_4547_b200 as srht
+from paper_0812_4547_b200 import _lib
+
+n, d, r = [int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (1 << 20, 512, 8192))]
+c = d + 1
+M = torch.empty((c, n), dtype=torch.float32, device="cuda").t()
+srht.gen_uniform(0, 0, M)
+plan = srht.Plan(n, d, r, 0)
+ws = plan.workspace(c)
+out = torch.empty((c, r), device="cuda").t()
+lib = _lib.load()
+tr = torch.zeros(3 * 64 * 8, dtype=torch.int64, device="cuda")
+lib.srht_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
+for _ in range(3):
+    plan.sketch_columns(M, out=out, workspace=ws)
+torch.cuda.synchronize()
+lib.srht_debug_set_trace(ctypes.c_void_p(0))
+print("kernel:", lib.srht_debug_last_kernel(), "shape", n, d, r)
+t = tr.cpu().numpy().reshape(3, 64, 8).astype(np.float64)
+order = [0, 6, 1, 2, 3, 4, 5]
+pn = ["TMA wait", "R1 LDS+signs+quarters", "R1 stage 12", "bar1+stage 13+STS", "bar2+R2 LDS+stages", "R2 last stage+STS+arrive"]
+for g in range(2):
+    rows = t[g, g::2][:30]
+    rows = rows[rows[:, 0] > 0]
+    print("producer group %d: tile-to-tile %.0f cycles (median, own tiles)" % (g, np.median(np.diff(rows[:, 0]))))
+    for k in range(6):
+        print("   %-26s %7.0f" % (pn[k], np.median(rows[:, order[k + 1]] - rows[:, order[k]])))
+    print("   %-26s %7.0f" % ("to next tile", np.median(rows[1:, 0] - rows[:-1, 5])))
+rows = t[2][t[2][:, 0] > 0]
+print("consumer t0: tile-to-tile %.0f" % np.median(np.diff(rows[:, 0])))
+for k, nm in enumerate(["READY wait+1st LDTM", "gather", "refill (last warp only)"]):
+    print("   %-22s %7.0f" % (nm, np.median(rows[:, k + 1] - rows[:, k])))
+# cross-role: when does the producer finish tile f vs consumer start it
+fin = {f: t[f % 2, f - 16, 5] for f in range(16, 80) if t[f % 2, f - 16, 5] > 0}

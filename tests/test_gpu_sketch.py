@@ -139,6 +139,52 @@ def _csc_dev(colptr, rowidx, vals, shape):
                    torch.from_numpy(np.asarray(vals, dtype=np.float32)).cuda(), shape)
 
 
+def check_fp64_mode(got, ref, M):
+    """FP64-accumulation mode: each output is the FP64 sum rounded once to FP32, so it is
+    within one FP32 spacing of the exact sketch (plus an FP64-level absolute term for
+    entries that cancel to ~0)."""
+    got = np.asarray(got, dtype=np.float64)
+    ulp = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+    floor = 1e-12 * math.sqrt(M.shape[0]) * np.max(np.abs(M), axis=0)
+    err = np.abs(got - ref)
+    assert np.all(err <= ulp + floor[None, :] + 1e-300), float((err / (ulp + floor[None, :] + 1e-300)).max())
+
+
+@pytest.mark.parametrize("n,c,r,seed", [
+    (4096, 17, 256, 0),        # config 1 shape
+    (1000, 3, 100, 1),         # ragged, r not a power of two
+    (1, 1, 1, 3),              # n = 1
+    (300000, 2, 2000, 7),      # several slabs: FP64 partials + FP64 reduce
+    (1 << 21, 2, 16384, 9),    # B = 2^14, two slabs
+    (70000, 2, 20000, 10),     # several sample groups
+])
+def test_fp64_mode_dense_parity(lib, n, c, r, seed):
+    from oracle import srht as osr
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, c)).astype(np.float32)
+    plan = lib.Plan(n, c - 1, r, seed, accum="fp64")
+    SM = plan.sketch_columns(to_dev(M), workspace=plan.workspace(c)).cpu().numpy()
+    ref = osr.sketch(M.astype(np.float64), seed, r)
+    check_fp64_mode(SM, ref, M)
+
+
+def test_fp64_mode_csc_and_batched(lib):
+    from oracle import srht as osr
+    n, ncols, per, r = 300000, 3, 3000, 2048
+    colptr, rowidx, vals = workloads.csc_lognormal(1, n, ncols, per)
+    dense = workloads.csc_to_dense(colptr, rowidx, vals, n, ncols)
+    plan = lib.Plan(n, ncols - 1, r, 5, accum="fp64")
+    SM = plan.sketch_columns(_csc_dev(colptr, rowidx, vals, (n, ncols)), workspace=plan.workspace(ncols)).cpu().numpy()
+    check_fp64_mode(SM, osr.sketch(dense, 5, r), dense.astype(np.float32))
+    batch, n, c, r = 5, 3000, 4, 256
+    M = np.random.default_rng(3).random((n, batch * c), dtype=np.float32)
+    plan = lib.Plan(n, c - 1, r, 13, batch=batch, accum="fp64")
+    out = plan.sketch_batched(to_dev(M)).cpu().numpy()
+    for p in range(batch):
+        check_fp64_mode(out[p].T, osr.sketch(M[:, p * c:(p + 1) * c].astype(np.float64), 13, r, p=p),
+                        M[:, p * c:(p + 1) * c])
+
+
 def lib_csc(*a):
     import paper_0812_4547_b200 as m
     return m.CSC(*a)
