@@ -229,6 +229,7 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       vp.scale = P->scale;
       vp.partials = sp.partials;
       vp.trace = srht::g_debug_trace;
+      vp.debug = srht::g_debug_mode;
       const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
       if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
       cudaError_t e = srht::launch_sketch_tma(P, vp, st);

@@ -122,6 +122,7 @@ struct V3Params {
   float scale;
   float* partials;        // [S_act][total_cols][r] when S_act > 1
   unsigned long long* trace;  // experiment phase timestamps (srht_debug_set_trace), else null
+  int debug;                  // experiment knock-outs (srht_debug_set_mode, debug build), else 0
 };
 cudaError_t launch_sketch_tma(const srht_plan* P, const V3Params& vp, cudaStream_t stream);
 int v3_mid(int x);  // kernel-v3 z layout (host side, for the slot layout)

@@ -216,13 +216,15 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
   }
 }
 
-// Experiment tracing (TR = true only when srht_debug_set_trace gave a buffer): clock64 at
-// phase boundaries of CTA 0, for flat tiles 16..79; see scripts/v3_trace.py.
+// Experiment variants (DBG != 0 only for srht_debug_set_trace / srht_debug_set_mode; results
+// are wrong for the knock-outs): bit 0 = clock64 at phase boundaries of CTA 0 for flat tiles
+// 16..79 (scripts/v3_trace.py); bit 1 = consumers skip the gather loads; bit 2 = producers
+// skip the butterflies; bit 3 = producers skip the shared-memory loads/stores of both rounds.
 #define V3_TRACE(role, k, pt)                                                            \
-  if (TR && blockIdx.x == 0 && (k) >= 16 && (k) < 80)                                    \
+  if ((DBG & 1) && blockIdx.x == 0 && (k) >= 16 && (k) < 80)                             \
     P.trace[((size_t)(role) * 64 + ((k) - 16)) * 8 + (pt)] = clock64();
 
-template <int RPT, bool TR>
+template <int RPT, int DBG>
 __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constant__ V3Params P) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint2* masks_s = reinterpret_cast<uint2*>(smem + MASK_OFF);
@@ -288,7 +290,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
 #pragma unroll
-        for (int h = 16 * q; h < 16 * q + 16; ++h) v[h] = *reinterpret_cast<const float2*>(buf + 2 * p + 256 * h);
+        for (int h = 16 * q; h < 16 * q + 16; ++h)
+          v[h] = (DBG & 8) ? make_float2((float)h, (float)p) : *reinterpret_cast<const float2*>(buf + 2 * p + 256 * h);
         // D: sign of (h, e) = bit 2(h & 15) + e of word h >> 4 (= word q).  Funnel shifts
         // keep the bit moves on the ALU pipe (IMAD.SHL would take FMA slots).
         const uint32_t w = q == 0 ? sg.x : q == 1 ? sg.y : q == 2 ? sg.z : sg.w;
@@ -298,22 +301,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
           v[h].x = flipf(v[h].x, __funnelshift_l(w, w, 31 - bt) & 0x80000000u);
           v[h].y = flipf(v[h].y, __funnelshift_l(w, w, 30 - bt) & 0x80000000u);
         }
-        fwht_quarter(v, q);  // row bit 0 (pair) and bits 8..11 (h bits 0..3)
+        if (!(DBG & 4)) fwht_quarter(v, q);  // row bit 0 (pair) and bits 8..11 (h bits 0..3)
       }
       if (p == 0) { V3_TRACE(g, f, 1) }
 #pragma unroll
       for (int m = 0; m < 64; ++m)
-        if (!(m & 16)) bfly<16>(v, m);  // row bit 12
+        if (!(m & 16) && !(DBG & 4)) bfly<16>(v, m);  // row bit 12
       if (p == 0) { V3_TRACE(g, f, 2) }
       bar_sync(BAR_GRP0 + g, 128);  // every raw row of the tile has been read
       // row bit 13, each result stored as soon as it is final: mid(x) = p + 130 (2h + e)
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
-        bfly<32>(v, m);
-        buf[p + ROWW * (2 * m)] = v[m].x;
-        buf[p + ROWW * (2 * m + 1)] = v[m].y;
-        buf[p + ROWW * (2 * (m + 32))] = v[m + 32].x;
-        buf[p + ROWW * (2 * (m + 32) + 1)] = v[m + 32].y;
+        if (!(DBG & 4)) bfly<32>(v, m);
+        if (!(DBG & 8)) {
+          buf[p + ROWW * (2 * m)] = v[m].x;
+          buf[p + ROWW * (2 * m + 1)] = v[m].y;
+          buf[p + ROWW * (2 * (m + 32))] = v[m + 32].x;
+          buf[p + ROWW * (2 * (m + 32) + 1)] = v[m + 32].y;
+        }
       }
       if (p == 0) { V3_TRACE(g, f, 3) }
       bar_sync(BAR_GRP0 + g, 128);
@@ -322,18 +327,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
 #pragma unroll
-        for (int m = 16 * q; m < 16 * q + 16; ++m) v[m] = *reinterpret_cast<const float2*>(rowp + 2 * m);
-        fwht_quarter(v, q);  // row bit 1 (pair) and bits 2..5 (m bits 0..3)
+        for (int m = 16 * q; m < 16 * q + 16; ++m)
+          v[m] = (DBG & 8) ? make_float2(v[m].y, v[m].x) : *reinterpret_cast<const float2*>(rowp + 2 * m);
+        if (!(DBG & 4)) fwht_quarter(v, q);  // row bit 1 (pair) and bits 2..5 (m bits 0..3)
       }
 #pragma unroll
       for (int m = 0; m < 64; ++m)
-        if (!(m & 16)) bfly<16>(v, m);  // row bit 6
+        if (!(m & 16) && !(DBG & 4)) bfly<16>(v, m);  // row bit 6
       if (p == 0) { V3_TRACE(g, f, 4) }
 #pragma unroll
       for (int m = 0; m < 32; ++m) {  // row bit 7, then z = H_B D x stored in place
-        bfly<32>(v, m);
-        *reinterpret_cast<float2*>(rowp + 2 * m) = v[m];
-        *reinterpret_cast<float2*>(rowp + 2 * (m + 32)) = v[m + 32];
+        if (!(DBG & 4)) bfly<32>(v, m);
+        if (!(DBG & 8)) {
+          *reinterpret_cast<float2*>(rowp + 2 * m) = v[m];
+          *reinterpret_cast<float2*>(rowp + 2 * (m + 32)) = v[m + 32];
+        } else if (v[m].x == 1.2345f) {  // keep the values live
+          rowp[m] = v[m + 32].y;
+        }
       }
       bar_arrive(BAR_READY0 + b, 384);
       if (p == 0) { V3_TRACE(g, f, 5) }
@@ -399,8 +409,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
               const int q = 2 * k + i;
               // word = lo | hi << 17 (15-bit word offsets; bits 15, 16 clear), so the high
               // sample's byte offset is w >> 15
-              const float z = (i & 1) ? *reinterpret_cast<const float*>(reinterpret_cast<const char*>(buf) + (wk[i >> 1] >> 15))
-                                      : buf[wk[i >> 1] & 0x7fffu];
+              const float z = (DBG & 2) ? __uint_as_float(wk[i >> 1] & 0x3fffffffu)
+                              : (i & 1) ? *reinterpret_cast<const float*>(reinterpret_cast<const char*>(buf) + (wk[i >> 1] >> 15))
+                                        : buf[wk[i >> 1] & 0x7fffu];
               const uint32_t mw = q < 32 ? mk.x : mk.y;
               acc[q] = flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u) + z;
             }
@@ -453,21 +464,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
   }
 }
 
-template <int RPT, bool TR>
-cudaError_t launch_tr(const V3Params& vp, int grid, cudaStream_t stream) {
+template <int RPT, int DBG>
+cudaError_t launch_dbg(const V3Params& vp, int grid, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
     const cudaError_t e =
-        cudaFuncSetAttribute(k_sketch_tma<RPT, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_sketch_tma<RPT, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_sketch_tma<RPT, TR><<<grid, NTHREADS, SMEM_BYTES, stream>>>(vp);
+  k_sketch_tma<RPT, DBG><<<grid, NTHREADS, SMEM_BYTES, stream>>>(vp);
   return cudaGetLastError();
 }
 template <int RPT>
 cudaError_t launch_rpt(const V3Params& vp, int grid, cudaStream_t stream) {
-  return vp.trace ? launch_tr<RPT, true>(vp, grid, stream) : launch_tr<RPT, false>(vp, grid, stream);
+  const int dbg = (vp.trace ? 1 : 0) | (vp.debug << 1);
+#ifdef SRHT_WS_DEBUG
+  if constexpr (RPT >= 32) {
+    switch (dbg) {
+      case 2: return launch_dbg<RPT, 2>(vp, grid, stream);
+      case 4: return launch_dbg<RPT, 4>(vp, grid, stream);
+      case 6: return launch_dbg<RPT, 6>(vp, grid, stream);
+      case 8: return launch_dbg<RPT, 8>(vp, grid, stream);
+      case 10: return launch_dbg<RPT, 10>(vp, grid, stream);
+      case 12: return launch_dbg<RPT, 12>(vp, grid, stream);
+      case 14: return launch_dbg<RPT, 14>(vp, grid, stream);
+      default: break;
+    }
+  }
+#endif
+  return dbg & 1 ? launch_dbg<RPT, 1>(vp, grid, stream) : launch_dbg<RPT, 0>(vp, grid, stream);
 }
 
 }  // namespace v3
