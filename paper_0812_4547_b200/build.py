@@ -55,6 +55,25 @@ def build_debug():
     return out
 
 
+def build_variant(name, defines):
+    """Experiment build: lib<name>.so with extra -D defines (A/B runs via SRHT_LIB=lib<name>.so)."""
+    os.makedirs(OBJ, exist_ok=True)
+    out = os.path.join(PKG, "lib%s.so" % name)
+    objs = []
+    for src in SOURCES:
+        o = os.path.join(OBJ, "%s_%s.o" % (name, os.path.splitext(src)[0]))
+        cmd = [NVCC] + ARCH + FLAGS + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, src), "-o", o]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr)
+        objs.append(o)
+    r = subprocess.run([NVCC] + ARCH + ["-shared", "-o", out] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return out
+
+
 def build(verbose=False, force=False):
     os.makedirs(OBJ, exist_ok=True)
     if force:

@@ -391,7 +391,10 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
     // slab) near 3% of the input, and slabs small enough to load-balance.
     const int64_t NB2 = N >> 14;
     int lj2 = 0;
-    while ((int64_t(1) << lj2) < 64 * r / (1 << 14) && lj2 < 6) ++lj2;
+#ifndef SRHT_V3_MAX_LOGJ
+#define SRHT_V3_MAX_LOGJ 6
+#endif
+    while ((int64_t(1) << lj2) < 64 * r / (1 << 14) && lj2 < SRHT_V3_MAX_LOGJ) ++lj2;
     while ((int64_t(1) << lj2) > NB2) --lj2;
     P->log_j2 = lj2;
     P->J2 = int64_t(1) << lj2;

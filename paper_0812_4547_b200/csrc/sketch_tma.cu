@@ -49,7 +49,7 @@ constexpr int MASK_OFF = SIGN_OFF + NBUF * 2048;
 constexpr int CTRL_OFF = MASK_OFF + V3_MAX_LOGJ * NCONS * 8;
 constexpr int SMEM_BYTES = CTRL_OFF + 256;  // mbarriers [0,24), TMEM address [32,36), slot states [64,..)
 
-enum { BAR_READY0 = 1, BAR_GRP0 = 4, BAR_CONS = 6, BAR_EMPTY0 = 7 };  // named barriers (0 = __syncthreads)
+enum { BAR_READY0 = 1, BAR_GRP0 = 4, BAR_CONS = 6 };  // named barriers (0 = __syncthreads)
 
 __host__ __device__ constexpr int mid(int x) { return ((x >> 1) & 127) + ROWW * ((x & 1) | ((x >> 8) << 1)); }
 
@@ -165,19 +165,16 @@ __device__ __forceinline__ const float* col_ptr(const V3Params& P, int col) {
 }
 
 // TMA issue.  Buffer slot b (tiles f = b, b+3, ...) keeps its own cursor: the next tile to
-// load into it.  When every consumer warp is done with tile f (named barrier EMPTY_b:
-// consumer warps 1..7 arrive without waiting, warp 0 syncs), consumer thread 0 refills
-// the slot: tile f+3's 64 KB of rows (L2 evict-first) plus its 2 KB of packed D bits (L2
-// evict-last: the sign words are re-read for every column), one mbarrier transaction; then
-// it advances the slot cursor by three active tiles and prefetches that tile (f+6) into L2.
+// load into it.  The consumer warp that finishes tile f last (shared-memory counter per
+// slot) refills the slot (measured faster than a named barrier on one refilling warp):
+// tile f+3's 64 KB of rows (L2 evict-first) plus its 2 KB of packed D bits (L2 evict-last:
+// the sign words are re-read for every column), one mbarrier transaction; then it advances
+// the slot cursor by three active tiles and prefetches that tile (f+6) into L2.
 // The cursors live in shared memory and cost the consumers no registers.
 struct SlotState {
   Cursor cur;   // next tile for this slot
   int count;    // consumer warps done with the slot's current tile (atomic refill)
 };
-#ifndef V3_REFILL_BARRIER
-#define V3_REFILL_BARRIER 0
-#endif
 #ifndef V3_L2_HINTS
 #define V3_L2_HINTS 1
 #endif
@@ -434,15 +431,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
             }
           }
           if (c == 0) { V3_TRACE(2, f, 2) }
-#if V3_REFILL_BARRIER
-          // every consumer warp done with buffer b -> consumer thread 0 refills it
-          if (wc == 0) {
-            bar_sync(BAR_EMPTY0 + b, NCONS);
-            if (c == 0) tma_issue(P, slots[b], b, smem);
-          } else {
-            bar_arrive(BAR_EMPTY0 + b, NCONS);
-          }
-#else
           // the last consumer warp done with buffer b refills it (no consumer-wide barrier)
           __syncwarp();
           if ((c & 31) == 0) {
@@ -452,7 +440,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
               tma_issue(P, slots[b], b, smem);
             }
           }
-#endif
           if (c == 0) { V3_TRACE(2, f, 3) }
           ++f;
         } else {
