@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="columns", choices=["columns", "rows"],
+                    help="multi-GPU partition of [A|b]: column ranges + all-gather (default) or "
+                         "row ranges + one FP64 all-reduce of the partial sums")
     return ap.parse_args()
 
 
@@ -269,10 +272,22 @@ def main():
         return bench_sparse(args, cfg, srht, _lib, world, rank, device)
     n, d, r, seed = cfg["n"], cfg["d"], cfg["r"], workloads.SEED
     c = d + 1
-    c0, c1 = column_range(c, world, rank)
-    cl = c1 - c0
-    Ml = build_dense_shard(cfg, c0, c1, seed, device, srht)
+    rows_mode = args.shard == "rows"
     plan = srht.Plan(n, d, r, seed)
+    if rows_mode:
+        # every rank holds rows [row0, row1) of all c columns (Uniform[0,1) from rank-specific
+        # streams: the timing does not depend on the values)
+        from paper_0812_4547_b200 import dist as sdist
+        row0, row1 = sdist.row_range(n, world, rank, plan.row_shard_rows())
+        c0, c1, cl = 0, c, c
+        Ml = torch.empty((c, row1 - row0), dtype=torch.float32, device=device).t()
+        if row1 > row0:
+            srht.gen_uniform(seed, 1000003 * (rank + 1), Ml)
+        torch.cuda.synchronize()
+    else:
+        c0, c1 = column_range(c, world, rank)
+        cl = c1 - c0
+        Ml = build_dense_shard(cfg, c0, c1, seed, device, srht)
     ws = plan.workspace(cl)
     stream = torch.cuda.current_stream(device)
     lib = _lib.load()
@@ -283,8 +298,19 @@ def main():
     else:
         full_out = torch.empty((c, r), dtype=torch.float32, device=device).t()
 
+    part_buf = torch.empty((c, r), dtype=torch.float64, device=device).t() if rows_mode else None
+
     def step():
-        if world > 1:
+        if rows_mode:
+            if Ml.shape[0]:
+                plan.sketch_rows_partial(Ml, row0, out=part_buf, workspace=ws)
+            else:
+                part_buf.zero_()
+            if world > 1:
+                dist.all_reduce(part_buf.t(), op=dist.ReduceOp.SUM)
+            torch.mul(part_buf, 1.0 / r ** 0.5, out=part_buf)
+            full_out.copy_(part_buf)
+        elif world > 1:
             sdist.sketch_sharded(plan, Ml, c, out=full_out, workspace=ws)
         else:
             plan.sketch_columns(Ml, out=full_out, workspace=ws)
@@ -320,7 +346,8 @@ def main():
     value = total_in / (ms * 1e-3) / 1e9
     kname = last_kernel(lib)
     peak, peak_kind, peaks = load_peaks()
-    alg_bytes_launch = 4.0 * n * cl + 4.0 * r * cl  # read the shard once, write r x c_l
+    # read the shard once, write r x c_l (rows mode: the shard's rows, FP64 r x c partials)
+    alg_bytes_launch = (4.0 * Ml.shape[0] * c + 8.0 * r * c) if rows_mode else (4.0 * n * cl + 4.0 * r * cl)
     achieved = alg_bytes_launch / (kms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": load_traffic(args.config, kname), "kernel": kname,
@@ -330,7 +357,7 @@ def main():
 
     # ---- e2e: the same sketch through the host-buffer C-ABI call ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not rows_mode:
         e2e = measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device)
 
     # ---- cpu_baseline: the oracle on the host cores (rank 0, N = 1 only) ----
@@ -345,7 +372,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "config%d_%s" % (args.config, cfg["name"]), "n": n, "d": d, "r": r,
-                       "columns": c, "input_bytes": total_in, "parallelism": "columns/%d" % world,
+                       "columns": c, "input_bytes": total_in,
+                       "parallelism": ("rows/%d" if rows_mode else "columns/%d") % world,
                        "l2": "inputs larger than L2 (no flush)" if total_in > 2 * 126e6 else "flushed"},
             "hbm_frac_of_measured": value / peak,
             "hbm_frac_of_8TBs": value / 8000.0,
@@ -353,7 +381,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * (2 if plan_has_reduce(plan) else 1),
+            "gpu_launches": args.steps * (2 if (plan_has_reduce(plan) or rows_mode) else 1),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -154,6 +154,27 @@ srht_status srht_sketch_batched(const srht_plan* plan, const srht_matrix* M,
                                 float* SM, void* workspace,
                                 size_t workspace_bytes, void* stream);
 
+/* ---- Row shards (data partitioned by rows across ranks) ----
+ * srht_row_shard_rows: the row granularity G of row shards for this plan (a
+ * power of two: the slab size of the kernels).
+ * srht_sketch_rows_partial: M holds rows [row0, row0 + M->rows) of the n-row
+ * matrix [A | b] (all of its columns); row0 must be a multiple of G and the
+ * shard must end at a multiple of G or at n.  Dense M is column-major with
+ * M->rows rows (ld >= M->rows); CSC M carries GLOBAL row indices in
+ * [row0, row0 + M->rows).  Writes the UNSCALED partial sums over these rows,
+ *     part[t + j*ldp] = sum_{row0 <= i < row0+rows} (-1)^{popc(k_t & i)} sigma_i M[i, j]
+ * in FP64 (ldp >= r), for every column j.  By linearity the sketch is
+ * r^{-1/2} * (sum of the partials of a row partition), e.g. after one
+ * all-reduce (paper_0812_4547_b200.dist.sketch_row_sharded).  Single-problem
+ * plans only; EINVAL otherwise or on misaligned shards.  Workspace as for
+ * srht_sketch (srht_workspace_bytes covers both).  Asynchronous on `stream`. */
+int64_t srht_row_shard_rows(const srht_plan* plan);
+srht_status srht_sketch_rows_partial(const srht_plan* plan,
+                                     const srht_matrix* M, int64_t row0,
+                                     double* part, int64_t ldp,
+                                     void* workspace, size_t workspace_bytes,
+                                     void* stream);
+
 /* Same as srht_sketch_columns, but M's values, column pointers, row indices
  * and SM are HOST buffers (pinned or pageable).  Host->device copies, the
  * sketch and the device->host copy run inside the call, pipelined over column

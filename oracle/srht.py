@@ -135,6 +135,23 @@ def sketch(M, seed, r, p=0, n=None):
     return math.sqrt(N / r) * HDM[K]            # non-zero rows of S H_N, times D M
 
 
+def sketch_rows_partial(M_rows, row0, n, seed, r, p=0):
+    """Unscaled partial sums over rows [row0, row0 + len(M_rows)) of an n-row [A | b]:
+
+        P[t, j] = sum_{i in rows} (-1)^{popc(k_t & i)} sigma_i M[i, j]  (float64, (r, c)).
+
+    Written as the definition restricted to those rows: sqrt(r) times the sketch of the
+    n-row matrix that equals M_rows on them and is zero elsewhere (H~ D is linear,
+    P:311-312), so the sketch is r^{-1/2} times the sum over a row partition.
+    """
+    M_rows = np.asarray(M_rows, dtype=np.float64)
+    if M_rows.ndim == 1:
+        M_rows = M_rows[:, None]
+    full = np.zeros((int(n), M_rows.shape[1]), dtype=np.float64)
+    full[int(row0):int(row0) + M_rows.shape[0]] = M_rows
+    return math.sqrt(r) * sketch(full, seed, r, p=p)
+
+
 def sketch_problem(A, b, seed, r, p=0):
     """(H~ D A, H~ D b) with one shared plan (reading R7)."""
     A = np.asarray(A, dtype=np.float64)

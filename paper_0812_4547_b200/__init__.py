@@ -201,6 +201,28 @@ class Plan:
                                             _stream_ptr(self.device)), "srht_sketch_columns")
         return SM
 
+    def row_shard_rows(self):
+        """Row granularity of row shards (srht_row_shard_rows)."""
+        return int(self._lib.srht_row_shard_rows(self._h))
+
+    def sketch_rows_partial(self, M, row0, out=None, workspace=None):
+        """Unscaled FP64 partial sums of rows [row0, row0 + M.rows) of [A | b] (a row shard).
+
+        M holds the shard's rows (dense: the local rows; CSC: global row indices).  Returns a
+        column-major float64 (r, c) tensor; r^{-1/2} times the sum over a row partition is the
+        sketch (srht_sketch_rows_partial).
+        """
+        torch = _torch()
+        keep = []
+        dM = _describe(M, keep)
+        if out is None:
+            out = torch.empty((dM.cols, self.r), dtype=torch.float64, device=self.device).t()
+        ws, wsb = self._ws_args(dM.cols, workspace)
+        ld = int(out.stride(1)) if dM.cols > 1 else self.r
+        check(self._lib.srht_sketch_rows_partial(self._h, ctypes.byref(dM), int(row0), out.data_ptr(), ld, ws, wsb,
+                                                 _stream_ptr(self.device)), "srht_sketch_rows_partial")
+        return out
+
     def sketch_batched(self, M, out=None, workspace=None):
         """Batched problems: M has batch*c columns; returns (batch, c, r) (row t fastest)."""
         torch = _torch()

@@ -49,16 +49,19 @@ srht::ColSrc make_src(const srht_matrix* M, float* out, int64_t ldo) {
   return c;
 }
 
-size_t partial_bytes(const srht_plan* P, int64_t ncols) {
+// Workspace of srht_sketch* (and of srht_sketch_rows_partial when `shards`, which always goes
+// through the slab partials): per-slab partial sums of the widest slab geometry in use.
+size_t partial_bytes(const srht_plan* P, int64_t ncols, bool shards = false) {
   if (ncols <= 0) return 0;
+  const int64_t min_s = shards ? 1 : 2;
   if (P->flags & SRHT_PLAN_ACCUM_FP64) {  // FP64 partials of the v1 slab geometry
-    if (P->S_act <= 1) return 0;
+    if (P->S_act < min_s) return 0;
     const size_t b = (size_t)P->S_act * (size_t)ncols * (size_t)P->r * sizeof(double);
     return (b + 255) & ~size_t(255);
   }
-  int64_t S = P->S_act > 1 ? P->S_act : 0;
-  if (P->ws_ok && P->S_act2 > 1 && P->S_act2 > S) S = P->S_act2;
-  if (S <= 1) return 0;
+  int64_t S = P->S_act;
+  if (P->ws_ok && P->S_act2 > S) S = P->S_act2;
+  if (S < min_s) return 0;
   const size_t b = (size_t)S * (size_t)ncols * (size_t)P->r * sizeof(float);
   return (b + 255) & ~size_t(255);
 }
@@ -166,9 +169,22 @@ srht::SketchParams base_params(const srht_plan* P) {
   return sp;
 }
 
-srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_bytes, void* stream) {
+// Global slab range [lo, hi) of slabs of `slab_rows` rows that covers rows [row0, row0 + nrows).
+void slab_range(int64_t row0, int64_t nrows, int64_t slab_rows, int64_t S_total, int64_t& lo, int64_t& cnt) {
+  lo = row0 / slab_rows;
+  int64_t hi = (row0 + nrows + slab_rows - 1) / slab_rows;
+  if (hi > S_total) hi = S_total;
+  cnt = hi - lo;
+}
+
+// Launch the sketch of sp's columns over rows [row0, row0 + nrows) (whole columns: 0, n).
+// With sp.part_out set, the unscaled FP64 partial sums of those rows go to part_out
+// (row shards); otherwise r^{-1/2} * sum goes to the sources' outputs.
+srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_bytes, void* stream,
+                int64_t row0 = 0, int64_t nrows = -1) {
   if (sp.total_cols == 0) return SRHT_OK;
-  const size_t need = partial_bytes(P, sp.total_cols);
+  if (nrows < 0) nrows = P->n;
+  const size_t need = partial_bytes(P, sp.total_cols, sp.part_out != nullptr);
   if (need) {
     if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255)) return SRHT_EINVAL;
     sp.partials = static_cast<float*>(ws);
@@ -177,6 +193,9 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
   if (cudaGetDevice(&dev) != cudaSuccess) return SRHT_ECUDA;
   if (dev != P->device) return SRHT_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool part = sp.part_out != nullptr;
+  // kernel v1 / FP64 geometry: slabs of B * J rows
+  slab_range(row0, nrows, P->B * P->J, P->S_act, sp.s_lo, sp.S_act);
   if (P->flags & SRHT_PLAN_ACCUM_FP64) {
     sp.partials64 = static_cast<double*>(ws);
     sp.partials = nullptr;
@@ -184,33 +203,39 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
   }
   const bool batched = sp.cols_per_problem != INT64_MAX;
   if (P->ws_ok && !batched) {
-    // dense sources -> kernel v2; CSC sources -> kernel v1 (separate launches)
-    srht::ColSrc dense[2], csc[2];
+    // dense sources -> kernel v3 (or v2 for unaligned columns); any CSC source -> one
+    // kernel-v1 launch for every column (e.g. CSC A + dense b)
+    srht::ColSrc dense[2];
     int nd = 0, ncsc = 0;
     const int nsrc = sp.total_cols > sp.ncols0 ? 2 : 1;
     for (int i = 0; i < nsrc; ++i) {
       if (sp.src[i].ncols <= 0) continue;
-      if (sp.src[i].fmt == SRHT_DENSE) dense[nd++] = sp.src[i]; else csc[ncsc++] = sp.src[i];
+      if (sp.src[i].fmt == SRHT_DENSE) dense[nd++] = sp.src[i]; else ++ncsc;
     }
-    if (ncsc) {  // any CSC source: one kernel-v1 launch for every column (e.g. CSC A + dense b)
-      cudaError_t e = srht::launch_sketch(P, sp, st);
-      return e == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
-    }
-    bool v3 = nd && P->v3_ok && srht::g_kernel_force != 2;
+    if (ncsc || !nd) return srht::launch_sketch(P, sp, st) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+    // kernel v2/v3 geometry: slabs of 2^14 * J2 rows
+    int64_t s_lo2, S2;
+    slab_range(row0, nrows, (int64_t(1) << 14) * P->J2, P->S_act2, s_lo2, S2);
+    const int direct = (P->S_act2 == 1 && !part) ? 1 : 0;
+    srht::SketchParams rp = sp;  // the fixed-order slab reduction of this geometry
+    rp.src[0] = dense[0];
+    rp.src[1] = nd == 2 ? dense[1] : srht::ColSrc();
+    rp.ncols0 = dense[0].ncols;
+    rp.total_cols = dense[0].ncols + (nd == 2 ? dense[1].ncols : 0);
+    rp.S_act = S2;
+    rp.s_lo = s_lo2;
+    bool v3 = P->v3_ok && srht::g_kernel_force != 2 && rp.total_cols * S2 < (int64_t(1) << 31);
     for (int i = 0; i < nd; ++i) v3 = v3 && dense[i].vec;
-    int64_t ncol_all = 0;
-    for (int i = 0; i < nd; ++i) ncol_all += dense[i].ncols;
-    v3 = v3 && ncol_all * P->S_act2 < (int64_t(1) << 31);
+    const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
+    if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
+    cudaError_t e;
     if (v3) {
       srht::V3Params vp;
       std::memset(&vp, 0, sizeof(vp));
-      vp.src[0] = dense[0];
-      vp.ncols0 = dense[0].ncols;
-      vp.total_cols = dense[0].ncols;
-      if (nd == 2) {
-        vp.src[1] = dense[1];
-        vp.total_cols += dense[1].ncols;
-      }
+      vp.src[0] = rp.src[0];
+      vp.src[1] = rp.src[1];
+      vp.ncols0 = rp.ncols0;
+      vp.total_cols = rp.total_cols;
       vp.signs = P->d_signs3;
       vp.meta = P->d_meta3;
       vp.perm = P->d_perm3;
@@ -220,41 +245,27 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       vp.n = P->n;
       vp.J = P->J2;
       vp.n_sub = P->n_sub2;
-      vp.S_act = P->S_act2;
-      vp.n_items = vp.total_cols * P->S_act2;
+      vp.S_act = S2;
+      vp.n_items = vp.total_cols * S2;
       vp.n_items32 = (int)vp.n_items;
-      vp.S_act32 = (int)vp.S_act;
+      vp.S_act32 = (int)S2;
+      vp.s_lo32 = (int)s_lo2;
       vp.J32 = (int)vp.J;
       vp.n_sub32 = (int)vp.n_sub;
       vp.scale = P->scale;
       vp.partials = sp.partials;
+      vp.direct = direct;
       vp.trace = srht::g_debug_trace;
       vp.debug = srht::g_debug_mode;
-      const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
-      if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
-      cudaError_t e = srht::launch_sketch_tma(P, vp, st);
+      e = srht::launch_sketch_tma(P, vp, st);
       srht::g_last_kernel = 3;
-      if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot + 1], st);
-      if (e != cudaSuccess) return SRHT_ECUDA;
-      if (P->S_act2 > 1) {
-        srht::SketchParams rp = sp;
-        rp.src[0] = vp.src[0];
-        rp.src[1] = vp.src[1];
-        rp.ncols0 = vp.ncols0;
-        rp.total_cols = vp.total_cols;
-        rp.S_act = P->S_act2;
-        if (srht::launch_reduce(rp, 14 + P->log_j2, st) != cudaSuccess) return SRHT_ECUDA;
-      }
-    } else if (nd) {
+    } else {
       srht::WsParams wp;
       std::memset(&wp, 0, sizeof(wp));
-      wp.src[0] = dense[0];
-      wp.ncols0 = dense[0].ncols;
-      wp.total_cols = dense[0].ncols;
-      if (nd == 2) {
-        wp.src[1] = dense[1];
-        wp.total_cols += dense[1].ncols;
-      }
+      wp.src[0] = rp.src[0];
+      wp.src[1] = rp.src[1];
+      wp.ncols0 = rp.ncols0;
+      wp.total_cols = rp.total_cols;
       wp.signs_ws = P->d_signs_ws;
       wp.meta = P->d_meta;
       wp.perm = P->d_perm;
@@ -262,43 +273,23 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       wp.n = P->n;
       wp.J = P->J2;
       wp.n_sub = P->n_sub2;
-      wp.S_act = P->S_act2;
-      wp.n_items = wp.total_cols * P->S_act2;
+      wp.S_act = S2;
+      wp.s_lo = s_lo2;
+      wp.n_items = wp.total_cols * S2;
       wp.scale = P->scale;
       wp.partials = sp.partials;
+      wp.direct = direct;
       wp.debug = srht::g_debug_mode;
       wp.trace = srht::g_debug_trace;
-      const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
-      if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
-      cudaError_t e = srht::launch_sketch_ws(P, wp, st);
+      e = srht::launch_sketch_ws(P, wp, st);
       srht::g_last_kernel = 2;
-      if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot + 1], st);
-      if (e != cudaSuccess) return SRHT_ECUDA;
-      if (P->S_act2 > 1) {
-        srht::SketchParams rp = sp;
-        rp.src[0] = wp.src[0];
-        rp.src[1] = wp.src[1];
-        rp.ncols0 = wp.ncols0;
-        rp.total_cols = wp.total_cols;
-        rp.S_act = P->S_act2;
-        if (srht::launch_reduce(rp, 14 + P->log_j2, st) != cudaSuccess) return SRHT_ECUDA;
-      }
     }
-    if (ncsc) {
-      srht::SketchParams cp = sp;
-      cp.src[0] = csc[0];
-      cp.ncols0 = csc[0].ncols;
-      cp.total_cols = csc[0].ncols;
-      if (ncsc == 2) {
-        cp.src[1] = csc[1];
-        cp.total_cols += csc[1].ncols;
-      }
-      if (srht::launch_sketch(P, cp, st) != cudaSuccess) return SRHT_ECUDA;
-    }
+    if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot + 1], st);
+    if (e != cudaSuccess) return SRHT_ECUDA;
+    if (!direct && srht::launch_reduce(rp, 14 + P->log_j2, st) != cudaSuccess) return SRHT_ECUDA;
     return SRHT_OK;
   }
-  cudaError_t e = srht::launch_sketch(P, sp, st);
-  return e == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+  return srht::launch_sketch(P, sp, st) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
 }
 
 }  // namespace
@@ -477,7 +468,7 @@ srht_status srht_plan_copy_signs(const srht_plan* P, int64_t problem, uint64_t* 
 
 size_t srht_workspace_bytes(const srht_plan* P, int64_t ncols) {
   if (!P) return 0;
-  return partial_bytes(P, ncols);
+  return partial_bytes(P, ncols, true);  // covers srht_sketch_rows_partial too
 }
 
 srht_status srht_sketch_columns(const srht_plan* P, const srht_matrix* M, float* SM, int64_t ldsm, void* ws,
@@ -521,6 +512,42 @@ srht_status srht_sketch_batched(const srht_plan* P, const srht_matrix* M, float*
   sp.total_cols = M->cols;
   sp.cols_per_problem = M->cols / P->batch;
   return run(P, sp, ws, ws_bytes, stream);
+}
+
+int64_t srht_row_shard_rows(const srht_plan* P) {
+  if (!P) return 0;
+  int64_t g = P->B * P->J;  // kernel v1 / FP64 slab
+  if (P->ws_ok) {
+    const int64_t g2 = (int64_t(1) << 14) * P->J2;  // kernel v2 / v3 slab
+    if (g2 > g) g = g2;
+  }
+  return g;  // both are powers of two, so the larger is a multiple of the smaller
+}
+
+srht_status srht_sketch_rows_partial(const srht_plan* P, const srht_matrix* M, int64_t row0, double* part,
+                                     int64_t ldp, void* ws, size_t ws_bytes, void* stream) {
+  if (!P || !M || !part || P->batch != 1 || ldp < P->r || row0 < 0) return SRHT_EINVAL;
+  if (M->rows < 1 || row0 + M->rows > P->n) return SRHT_EINVAL;
+  const int64_t g = srht_row_shard_rows(P);
+  if (row0 % g != 0 || ((row0 + M->rows) % g != 0 && row0 + M->rows != P->n)) return SRHT_EINVAL;
+  srht_matrix Mg = *M;  // the shard seen with global row indices
+  if (M->fmt == SRHT_DENSE) {
+    if (!valid_matrix(M)) return SRHT_EINVAL;
+    Mg.rows = P->n;
+    if (M->cols > 0) Mg.vals = M->vals - row0;  // never dereferenced outside [row0, row0 + rows)
+  } else {
+    // CSC shards carry global row indices in [row0, row0 + rows); validated as an n-row matrix
+    Mg.rows = P->n;
+    if (!valid_matrix(&Mg)) return SRHT_EINVAL;
+  }
+  srht::SketchParams sp = base_params(P);
+  sp.src[0] = make_src(&Mg, nullptr, P->r);
+  sp.ncols0 = M->cols;
+  sp.total_cols = M->cols;
+  sp.cols_per_problem = INT64_MAX;
+  sp.part_out = part;
+  sp.ldp = ldp;
+  return run(P, sp, ws, ws_bytes, stream, row0, M->rows);
 }
 
 // Undeclared test hook: copy the kernel-v2 consumer slot layout to the host.

@@ -74,12 +74,15 @@ struct SketchParams {
   int64_t J;
   int log_j;
   int64_t n_sub;
-  int64_t S_act;
+  int64_t S_act;              // slabs of this launch: global slabs s_lo .. s_lo + S_act - 1
+  int64_t s_lo;               // first global slab (row shards, srht_sketch_rows_partial); else 0
   int64_t groups;
   float scale;
   double scale_f64;           // r^{-1/2} in FP64 (slab reduction)
-  float* partials;            // [S_act][total_cols][r] when S_act > 1
-  double* partials64;         // FP64 mode: [S_act][total_cols][r] when S_act > 1
+  float* partials;            // [S_act][total_cols][r] when S_act > 1 or part_out
+  double* partials64;         // FP64 mode: [S_act][total_cols][r] when S_act > 1 or part_out
+  double* part_out;           // row-shard mode: unscaled FP64 partial sums, column j at part_out + j*ldp
+  int64_t ldp;
 };
 // FP64-accumulation parity mode (sketch_f64.cu), v1 slab geometry.
 cudaError_t launch_sketch_f64(const srht_plan* P, const SketchParams& sp, cudaStream_t stream);
@@ -94,10 +97,12 @@ struct WsParams {
   const uint32_t* meta;
   const int32_t* perm;
   int64_t r, n;
-  int64_t J, n_sub, S_act;
+  int64_t J, n_sub, S_act;  // S_act: slabs of this launch, global slabs s_lo ..
+  int64_t s_lo;
   int64_t n_items;        // total_cols * S_act
   float scale;
-  float* partials;        // [S_act][total_cols][r] when S_act > 1
+  float* partials;        // [S_act][total_cols][r] when S_act > 1 or direct == 0
+  int direct;             // 1: single slab, write r^{-1/2} * sum straight to the output
   int debug;              // experiment knock-outs (srht_debug_set_mode); 0 in production
   unsigned long long* trace;  // experiment phase timestamps (debug build only)
 };
@@ -116,11 +121,12 @@ struct V3Params {
   const uint2* masks;     // plan d_masks3
   int log_j;
   int64_t r, n;
-  int64_t J, n_sub, S_act;
+  int64_t J, n_sub, S_act;  // S_act: slabs of this launch, global slabs s_lo ..
   int64_t n_items;        // total_cols * S_act
-  int n_items32, S_act32, J32, n_sub32;  // the same, 32-bit (checked on the host)
+  int n_items32, S_act32, J32, n_sub32, s_lo32;  // the same, 32-bit (checked on the host)
   float scale;
-  float* partials;        // [S_act][total_cols][r] when S_act > 1
+  float* partials;        // [S_act][total_cols][r] when S_act > 1 or direct == 0
+  int direct;             // 1: single slab, write r^{-1/2} * sum straight to the output
   unsigned long long* trace;  // experiment phase timestamps (srht_debug_set_trace), else null
   int debug;                  // experiment knock-outs (srht_debug_set_mode, debug build), else 0
 };

@@ -99,7 +99,8 @@ __global__ void __launch_bounds__((1 << LOG_B) / 32, 512 / ((1 << LOG_B) / 32))
   int64_t item = blockIdx.x;
   const int64_t g = item % P.groups;
   item /= P.groups;
-  const int64_t s = item % P.S_act;
+  const int64_t sl = item % P.S_act;  // slab of this launch
+  const int64_t s = P.s_lo + sl;      // global slab
   const int64_t col = item / P.S_act;
   const bool second = col >= P.ncols0;
   const ColSrc& cs = second ? P.src[1] : P.src[0];
@@ -255,14 +256,14 @@ __global__ void __launch_bounds__((1 << LOG_B) / 32, 512 / ((1 << LOG_B) / 32))
   }
 
   // ---- epilogue ----
-  if (P.S_act == 1) {
+  if (P.S_act == 1 && !P.part_out) {
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int64_t t = t0 + (int64_t)q * T + tid;
       if (t < P.r) cs.out[lc * cs.ldo + t] = acc[q] * P.scale;
     }
   } else {
-    float* __restrict__ part = P.partials + (s * P.total_cols + col) * P.r;
+    float* __restrict__ part = P.partials + (sl * P.total_cols + col) * P.r;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int64_t t = t0 + (int64_t)q * T + tid;
@@ -283,7 +284,11 @@ __global__ void k_reduce_slabs(const __grid_constant__ SketchParams P, int slab_
   double sum = 0.0;
   for (int64_t s = 0; s < P.S_act; ++s) {
     const float v = P.partials[(s * P.total_cols + col) * P.r + t];
-    sum += (double)flip(v, __popc(ks & (uint32_t)s) & 1u);
+    sum += (double)flip(v, __popc(ks & (uint32_t)(P.s_lo + s)) & 1u);
+  }
+  if (P.part_out) {  // row shard: unscaled partial, summed across shards by the caller
+    P.part_out[col * P.ldp + t] = sum;
+    return;
   }
   const bool second = col >= P.ncols0;
   const ColSrc& cs = second ? P.src[1] : P.src[0];
@@ -346,7 +351,7 @@ cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream
   }
   if (slot >= 0) cudaEventRecord(g_prof.ev[2 * slot + 1], stream);
   g_last_kernel = 1;
-  if (e != cudaSuccess || sp.S_act == 1) return e;
+  if (e != cudaSuccess || (sp.S_act == 1 && !sp.part_out)) return e;
   return launch_reduce(sp, P->log_b + P->log_j, stream);
 }
 

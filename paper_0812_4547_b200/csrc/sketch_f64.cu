@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(T64) k_sketch_f64(const __grid_constant__ Sket
   int64_t item = blockIdx.x;
   const int64_t g = item % groups;
   item /= groups;
-  const int64_t s = item % P.S_act;
+  const int64_t sl = item % P.S_act;  // slab of this launch
+  const int64_t s = P.s_lo + sl;      // global slab
   const int64_t col = item / P.S_act;
   const bool second = col >= P.ncols0;
   const ColSrc& cs = second ? P.src[1] : P.src[0];
@@ -154,14 +155,14 @@ __global__ void __launch_bounds__(T64) k_sketch_f64(const __grid_constant__ Sket
     __syncthreads();
   }
 
-  if (P.S_act == 1) {
+  if (P.S_act == 1 && !P.part_out) {
 #pragma unroll
     for (int q = 0; q < RPT64; ++q) {
       const int64_t t = t0 + (int64_t)q * T64 + tid;
       if (t < P.r) cs.out[lc * cs.ldo + t] = (float)(acc[q] * P.scale_f64);
     }
   } else {
-    double* __restrict__ part = P.partials64 + (s * P.total_cols + col) * P.r;
+    double* __restrict__ part = P.partials64 + (sl * P.total_cols + col) * P.r;
 #pragma unroll
     for (int q = 0; q < RPT64; ++q) {
       const int64_t t = t0 + (int64_t)q * T64 + tid;
@@ -180,7 +181,11 @@ __global__ void k_reduce_slabs_f64(const __grid_constant__ SketchParams P, int s
   double sum = 0.0;
   for (int64_t s = 0; s < P.S_act; ++s) {
     const double v = P.partials64[(s * P.total_cols + col) * P.r + t];
-    sum += (__popc(ks & (uint32_t)s) & 1) ? -v : v;
+    sum += (__popc(ks & (uint32_t)(P.s_lo + s)) & 1) ? -v : v;
+  }
+  if (P.part_out) {  // row shard: unscaled partial
+    P.part_out[col * P.ldp + t] = sum;
+    return;
   }
   const bool second = col >= P.ncols0;
   const ColSrc& cs = second ? P.src[1] : P.src[0];
@@ -227,7 +232,7 @@ cudaError_t launch_sketch_f64(const srht_plan* P, const SketchParams& sp, cudaSt
   }
   if (slot >= 0) cudaEventRecord(g_prof.ev[2 * slot + 1], stream);
   g_last_kernel = 4;
-  if (e != cudaSuccess || sp.S_act == 1) return e;
+  if (e != cudaSuccess || (sp.S_act == 1 && !sp.part_out)) return e;
   const int64_t zc = (sp.total_cols + 65534) / 65535;
   dim3 grid((unsigned)((sp.r + 255) / 256), (unsigned)(sp.total_cols < 65535 ? sp.total_cols : 65535), (unsigned)zc);
   k_reduce_slabs_f64<<<grid, 256, 0, stream>>>(sp, P->log_b + P->log_j);

@@ -132,7 +132,7 @@ struct Cursor {
 __device__ __forceinline__ void cursor_item(const V3Params& P, Cursor& c) {
   if (c.it >= P.n_items32) return;
   c.col = c.it / P.S_act32;
-  c.s = c.it - c.col * P.S_act32;
+  c.s = P.s_lo32 + c.it - c.col * P.S_act32;  // global slab
   const int rest = P.n_sub32 - c.s * P.J32;
   c.cnt = rest < P.J32 ? rest : P.J32;
   c.np = 1 << (32 - __clz(c.cnt - 1));  // next power of two >= cnt (cnt >= 1)
@@ -463,8 +463,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
           const int t = pk & 0xffff;
           const uint32_t kmid = (uint32_t)pk >> 16;
           const float a = flipf(acc[q], (uint32_t)(__popc(kmid & jlast) & 1) << 31);
-          if (P.S_act == 1) outp[lc * ldo + t] = a * P.scale;
-          else P.partials[((int64_t)s * P.total_cols + col) * P.r + t] = a;
+          if (P.direct) outp[lc * ldo + t] = a * P.scale;
+          else P.partials[((int64_t)(s - P.s_lo32) * P.total_cols + col) * P.r + t] = a;
         }
         acc[q] = 0.f;
       }

@@ -117,7 +117,7 @@ __device__ __forceinline__ void cursor_item(const WsParams& P, Cursor& c) {
   c.valid = c.it < P.n_items;
   if (!c.valid) return;
   c.col = (int)(c.it / P.S_act);
-  c.s = (int)(c.it - (int64_t)c.col * P.S_act);
+  c.s = (int)(P.s_lo + c.it - (int64_t)c.col * P.S_act);  // global slab
   const int64_t j0 = (int64_t)c.s * P.J;
   c.cnt = (int)((P.n_sub - j0 < P.J) ? P.n_sub - j0 : P.J);
   int L = 0;
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
     const char* tb1 = tb0 + TILE_BYTES;
     for (int64_t it = blockIdx.x; it < P.n_items; it += gridDim.x) {
       const int col = (int)(it / P.S_act);
-      const int s = (int)(it - (int64_t)col * P.S_act);
+      const int s = (int)(P.s_lo + it - (int64_t)col * P.S_act);  // global slab
       const int64_t j0 = (int64_t)s * P.J;
       const int cnt = (int)((P.n_sub - j0 < P.J) ? P.n_sub - j0 : P.J);
       int L = 0;
@@ -410,8 +410,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
         if (t >= 0) {
           const uint32_t kmid = __brev(mrow[q * NCONS]) & (uint32_t)(P.J - 1);
           const float a = flipf(acc[q], (uint32_t)(__popc(kmid & jlast) & 1) << 31);
-          if (P.S_act == 1) outp[lc * ldo + t] = a * P.scale;
-          else P.partials[((int64_t)s * P.total_cols + col) * P.r + t] = a;
+          if (P.direct) outp[lc * ldo + t] = a * P.scale;
+          else P.partials[((int64_t)(s - P.s_lo) * P.total_cols + col) * P.r + t] = a;
         }
         acc[q] = 0.f;
       }

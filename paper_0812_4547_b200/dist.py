@@ -1,4 +1,4 @@
-"""Column-sharded SRHT across ranks (one process per GPU, torch.distributed).
+"""Column- and row-sharded SRHT across ranks (one process per GPU, torch.distributed).
 
 Columns of M = [A | b] are independent given the plan, and every rank derives
 the same D and kept rows from the same seed (R4-R6), so rank k sketches
@@ -9,6 +9,11 @@ are padded to ceil(c / world) columns for ``all_gather_into_tensor`` and
 compacted afterwards.  With the NCCL backend the gather runs over NVLink /
 NVSwitch; the tile and slab geometry depend only on (n, r), so the result is
 bit-identical to a single-GPU sketch.
+
+Row sharding (for data that arrives partitioned by rows): rank k
+holds rows [row0_k, row1_k) of every column, computes the unscaled FP64 partial sums
+of its rows (srht_sketch_rows_partial), and one all-reduce (SUM, FP64) adds them; by
+linearity of H~ D r^{-1/2} times the total is the sketch.
 """
 
 import hashlib
@@ -100,3 +105,35 @@ def sketch_sharded(plan, M_shard, total_cols, group=None, out=None, sketch_fn=No
         out.copy_(full.t())
         return out
     return full.t()
+
+
+def row_range(n, world, rank, granularity):
+    """Row shard [r0, r1) of n rows for `rank`: whole multiples of `granularity`, the last
+    rank also takes the tail (balanced over granules)."""
+    granules = -(-int(n) // int(granularity))
+    base, rem = divmod(granules, int(world))
+    g0 = rank * base + min(rank, rem)
+    g1 = g0 + base + (1 if rank < rem else 0)
+    return min(g0 * granularity, n), min(g1 * granularity, n)
+
+
+def sketch_row_sharded(plan, M_rows, row0, group=None, partial_fn=None, workspace=None):
+    """Sketch of a row-partitioned [A | b]: this rank's rows [row0, row0 + M_rows.rows).
+
+    plan:       srht Plan (same seed on every rank)
+    M_rows:     this rank's rows of every column (row_range with plan.row_shard_rows())
+    partial_fn: optional replacement for ``plan.sketch_rows_partial`` with the same contract
+                (the CPU/gloo tests plug in the oracle)
+    Returns the float32 (r, c) sketch (column-major) on every rank.
+    """
+    if M_rows.shape[0] == 0:  # a rank past the last granule contributes zeros
+        part = torch.zeros((M_rows.shape[1], plan.r), dtype=torch.float64, device=M_rows.device).t()
+    elif partial_fn is None:
+        part = plan.sketch_rows_partial(M_rows, row0, workspace=workspace)
+    else:
+        part = partial_fn(M_rows, row0)
+    if not part.t().is_contiguous():
+        part = part.t().contiguous().t()  # column-major (r, c)
+    flat = part.t()  # (c, r) view of the column-major buffer, contiguous
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return (part * (1.0 / float(plan.r) ** 0.5)).float()

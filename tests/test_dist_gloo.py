@@ -110,3 +110,66 @@ def test_digest_mismatch_detectable():
     for p in procs:
         p.join(timeout=60)
     assert res == [False, False]
+
+
+# ---- row sharding: partial sums per row shard, one all-reduce ----
+
+class OracleRowPlan:
+    """Stands in for srht.Plan for row shards on CPU: oracle partials, same contract."""
+
+    def __init__(self, n, r, seed):
+        self.n, self.r, self.seed = n, r, seed
+
+    def partial(self, M_rows, row0):
+        from oracle import srht as osr
+        P = osr.sketch_rows_partial(M_rows.numpy().astype(np.float64), row0, self.n, self.seed, self.r)
+        return torch.from_numpy(np.asfortranarray(P))
+
+
+def _row_worker(rank, world, port, n, c, r, seed, gran, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_0812_4547_b200.dist import row_range, sketch_row_sharded
+        rng = np.random.default_rng(321)
+        M = rng.standard_normal((n, c)).astype(np.float32)
+        r0, r1 = row_range(n, world, rank, gran)
+        plan = OracleRowPlan(n, r, seed)
+        full = sketch_row_sharded(plan, torch.from_numpy(M[r0:r1]), r0, partial_fn=plan.partial)
+        q.put((rank, full.contiguous().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,gran", [(300, 64), (256, 128), (100, 64)])
+def test_gloo_row_shards_match_single_process(n, gran):
+    c, r, seed, world = 3, 40, 9, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_row_worker, args=(k, world, port, n, c, r, seed, gran, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle import srht as osr
+    M = np.random.default_rng(321).standard_normal((n, c)).astype(np.float32)
+    ref = osr.sketch(M.astype(np.float64), seed, r)
+    for k in range(world):
+        np.testing.assert_allclose(res[k].astype(np.float64), ref, rtol=1e-6, atol=1e-6)
+        assert np.array_equal(res[k], res[0])  # every rank holds the same result
+
+
+def test_row_range_partition():
+    from paper_0812_4547_b200.dist import row_range
+    for n, gran in [(1 << 20, 1 << 14), (300, 64), (100, 64), ((1 << 20) + 5, 1 << 18)]:
+        for world in [1, 2, 3, 8]:
+            rr = [row_range(n, world, k, gran) for k in range(world)]
+            assert rr[0][0] == 0 and rr[-1][1] == n
+            for (a0, a1), (b0, b1) in zip(rr, rr[1:]):
+                assert a1 == b0
+            for a, b in rr:
+                assert (a % gran == 0 and (b % gran == 0 or b == n)) or a == b == n  # empty tail ranks

@@ -293,3 +293,82 @@ def test_ws_slot_layout(lib, n, r):
     banks = np.where(valid, ((meta & 0x1FFFF) // 4 % 32).astype(np.int64), -1).reshape(-1, 32)
     worst = max(np.bincount(row[row >= 0], minlength=32).max() if (row >= 0).any() else 0 for row in banks)
     assert worst <= 2, worst
+
+
+# ---- row shards: unscaled FP64 partials per shard, summed by the caller ----
+
+def _row_cuts(n, g, k):
+    """k shards of whole granules (the last takes the tail)."""
+    gran = -(-n // g)
+    cuts = [min(n, (gran * i // k) * g) for i in range(k)] + [n]
+    return [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
+
+
+@pytest.mark.parametrize("n,c,r,seed,ld_pad", [
+    ((3 << 20) + 777, 3, 8192, 21, 0),   # kernel v3 (aligned dense), ragged last shard
+    ((1 << 21) + 5, 2, 16384, 22, 1),    # ld = n + 1: kernel v2 path
+    (50000, 3, 700, 23, 0),              # small N: kernel v1 path (one slab: partials forced)
+])
+def test_row_shard_partials_dense(lib, n, c, r, seed, ld_pad):
+    import torch
+    from oracle import srht as osr
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, c)).astype(np.float32)
+    buf = torch.zeros((c, n + ld_pad), dtype=torch.float32)
+    buf[:, :n] = torch.from_numpy(M.T)
+    Md = buf.cuda().t()[:n]  # column-major, ld = n + ld_pad
+    plan = lib.Plan(n, c - 1, r, seed)
+    g = plan.row_shard_rows()
+    full = plan.sketch_columns(Md, workspace=plan.workspace(c)).cpu().numpy().astype(np.float64)
+    tot = np.zeros((r, c))
+    for a, b in _row_cuts(n, g, 3):
+        P = plan.sketch_rows_partial(Md[a:b], a, workspace=plan.workspace(c)).cpu().numpy()
+        ref = osr.sketch_rows_partial(M[a:b].astype(np.float64), a, n, seed, r)
+        bound = 1e-5 * math.sqrt(n) * np.max(np.abs(M), axis=0) * math.sqrt(r)
+        assert np.all(np.abs(P - ref) <= bound[None, :])
+        tot += P
+    scaled = (tot / math.sqrt(r)).astype(np.float32).astype(np.float64)
+    # same slab partials as the full sketch; only the FP64 association order differs
+    ulp = np.spacing(np.abs(full).astype(np.float32)).astype(np.float64)
+    assert np.all(np.abs(scaled - full) <= ulp)
+    check_close(scaled, osr.sketch(M.astype(np.float64), seed, r), M)
+
+
+def test_row_shard_csc_global_indices_and_fp64(lib):
+    from oracle import srht as osr
+    n, ncols, per, r = 300000, 3, 3000, 2048
+    colptr, rowidx, vals = workloads.csc_lognormal(4, n, ncols, per)
+    dense = workloads.csc_to_dense(colptr, rowidx, vals, n, ncols)
+    for accum in ("fp32", "fp64"):
+        plan = lib.Plan(n, ncols - 1, r, 6, accum=accum)
+        g = plan.row_shard_rows()
+        tot = np.zeros((r, ncols))
+        for a, b in _row_cuts(n, g, 2):
+            cp, ri, va = [0], [], []
+            for j in range(ncols):  # the shard's entries, global row indices
+                sel = slice(colptr[j], colptr[j + 1])
+                keep = (rowidx[sel] >= a) & (rowidx[sel] < b)
+                ri.extend(rowidx[sel][keep]); va.extend(vals[sel][keep]); cp.append(len(ri))
+            P = plan.sketch_rows_partial(_csc_dev(cp, ri, va, (b - a, ncols)), a,
+                                         workspace=plan.workspace(ncols)).cpu().numpy()
+            ref = osr.sketch_rows_partial(dense[a:b], a, n, 6, r)
+            bound = 1e-5 * math.sqrt(n) * np.max(np.abs(dense), axis=0) * math.sqrt(r)
+            assert np.all(np.abs(P - ref) <= bound[None, :])
+            if accum == "fp64":
+                assert np.all(np.abs(P - ref) <= 1e-9 * np.maximum(np.abs(ref), 1.0))
+            tot += P
+        check_close(tot / math.sqrt(r), osr.sketch(dense, 6, r), dense.astype(np.float32))
+
+
+def test_row_shard_invalid_arguments(lib):
+    import torch
+    n, r = (1 << 21), 1024
+    plan = lib.Plan(n, 1, r, 0)
+    g = plan.row_shard_rows()
+    M = torch.zeros((2, n), device="cuda").t()
+    with pytest.raises(lib.SrhtError):
+        plan.sketch_rows_partial(M[g // 2:g], g // 2)        # row0 not a multiple of G
+    with pytest.raises(lib.SrhtError):
+        plan.sketch_rows_partial(M[0:g + 3], 0)             # ends inside a granule, not at n
+    P = plan.sketch_rows_partial(M[g:], g)                  # ends at n: fine
+    assert P.dtype == torch.float64 and P.shape == (r, 2)

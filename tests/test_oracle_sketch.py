@@ -81,3 +81,31 @@ def test_linearity():
 def test_tiny_n(n):
     SM = srht.sketch(np.ones(n), 0, 2)
     assert SM.shape == (2, 1)
+
+
+def test_rows_partial_matches_closed_form():
+    # Row-shard partial against the closed form of the definition,
+    # entry by entry with explicit loops: P[t, j] = sum_{i in rows} (-1)^popc(k_t & i) sigma_i M[i, j].
+    n, r, seed, c = 23, 5, 3, 2
+    N = srht.padded_size(n)
+    rng = np.random.default_rng(11)
+    M = rng.standard_normal((n, c))
+    sigma = srht.plan_signs(seed, 0, N)
+    K = srht.plan_samples(seed, 0, N, r)
+    for row0, row1 in [(0, 8), (8, 23), (5, 6), (0, 23)]:
+        got = srht.sketch_rows_partial(M[row0:row1], row0, n, seed, r)
+        ref = np.zeros((r, c))
+        for t in range(r):
+            for i in range(row0, row1):
+                sgn = (-1.0) ** bin(int(K[t]) & i).count("1") * sigma[i]
+                ref[t] += sgn * M[i]
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_rows_partials_of_a_partition_sum_to_the_sketch():
+    # linearity across a row partition, scaled by r^{-1/2} (the all-reduce of row sharding)
+    n, r, seed = 300, 40, 7
+    M = np.random.default_rng(5).standard_normal((n, 3))
+    cuts = [0, 64, 128, 200, 300]
+    tot = sum(srht.sketch_rows_partial(M[a:b], a, n, seed, r) for a, b in zip(cuts, cuts[1:]))
+    np.testing.assert_allclose(tot / math.sqrt(r), srht.sketch(M, seed, r), rtol=1e-12, atol=1e-12)
