@@ -175,6 +175,38 @@ srht_status srht_sketch_rows_partial(const srht_plan* plan,
                                      void* workspace, size_t workspace_bytes,
                                      void* stream);
 
+/* ---- Gram matrices of sketches: the QP form of Section 3.4 ----
+ * For p < batch: G_p = SM_p^T SM_p (c x c, FP64, column-major, both triangles,
+ * G_p[i + j*ldg] at G + p*stride_g, ldg >= c) where SM_p is the r x c FP32
+ * column-major block at SM + p*stride_sm (ldsm >= r; for batch > 1 the strides
+ * must separate the blocks).  With SM_p = [SA | Sb] (srht_sketch*):
+ *     G_p = [[Q~, q~], [q~^T, Sb^T Sb]],  Q~ = (H~DA)^T H~DA,  q~ = (H~DA)^T H~Db,
+ * so min_{x>=0} ||SA x - Sb||^2 = min x^T Q~ x - 2 q~^T x + Sb^T Sb.  Products of
+ * the FP32 entries are exact in FP64 and accumulated in FP64.  All pointers are
+ * device pointers; asynchronous on `stream` (cudaStream_t as void*).         */
+srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM,
+                      int64_t ldsm, int64_t stride_sm, double* G, int64_t ldg,
+                      int64_t stride_g, void* stream);
+
+/* ---- NNLS on the Gram form (Algorithm 1 step 5, via P:570-590) ----
+ * For p < batch: x_p = argmin_{x >= 0} x^T Q x - 2 q^T x, i.e. the NNLS solution
+ * of min ||SA x - Sb|| when G_p = [[Q, q], [q^T, .]] = srht_gram([SA | Sb]) is
+ * (d+1) x (d+1) FP64 column-major at G + p*stride_g (ldg >= d+1).  Lawson-Hanson
+ * active set with the oracle's rules (reading R13: argmax dual entry,
+ * smallest-index ties, tol 1e-10 max|q|, degenerate entries skipped, <= 30 d
+ * outer iterations, x < 1e-14 snapped to 0); the passive-set solve is a
+ * Cholesky factorization of Q_PP (needs a full-column-rank SA, the generic case
+ * for r >= d+1).  x_p (d FP64) at x + p*stride_x; iters[p] (device, may be NULL)
+ * = outer iterations, or -1 (iteration cap), -2 (inner loop cap), -3 (Q_PP not
+ * positive definite).  One CTA per problem.  Workspace: the Cholesky factors
+ * when d > 160 (srht_nnls_workspace_bytes; 0 otherwise), 8-byte aligned.
+ * Device pointers; asynchronous on `stream`.                                  */
+size_t srht_nnls_workspace_bytes(int64_t d, int64_t batch);
+srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G,
+                           int64_t ldg, int64_t stride_g, double* x,
+                           int64_t stride_x, int32_t* iters, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* Same as srht_sketch_columns, but M's values, column pointers, row indices
  * and SM are HOST buffers (pinned or pageable).  Host->device copies, the
  * sketch and the device->host copy run inside the call, pipelined over column

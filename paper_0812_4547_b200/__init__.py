@@ -22,7 +22,7 @@ import numpy as np
 from . import _lib
 from ._lib import SRHT_CSC, SRHT_DENSE, SrhtMatrix, SrhtError, check
 
-__all__ = ["Plan", "CSC", "SrhtError", "colmajor", "gen_uniform", "padded_size", "library"]
+__all__ = ["Plan", "CSC", "SrhtError", "colmajor", "gen_uniform", "gram", "nnls_gram", "padded_size", "library"]
 
 CSC = namedtuple("CSC", ["colptr", "rowidx", "vals", "shape"])
 CSC.__doc__ = "Compressed sparse columns: int64 colptr[c+1], int32 rowidx[nnz] (sorted per column), float32 vals."
@@ -278,3 +278,53 @@ def gen_uniform(seed, stream0, out):
     check(lib.srht_gen_uniform(ctypes.c_uint64(seed), ctypes.c_uint64(stream0), rows, cols, out2.data_ptr(), ld,
                                _stream_ptr(out.device)), "srht_gen_uniform")
     return out
+
+
+def gram(SM):
+    """FP64 Gram matrices G = SM^T SM of sketches (srht_gram; the QP form of Section 3.4).
+
+    SM: column-major float32 CUDA tensor (r, c), or a (batch, c, r) tensor as returned by
+    Plan.sketch_batched.  Returns (c, c) or (batch, c, c) float64 (symmetric).
+    """
+    torch = _torch()
+    lib = _lib.load()
+    if not SM.is_cuda or SM.dtype != torch.float32:
+        raise ValueError("SM must be a float32 CUDA tensor")
+    if SM.dim() == 3:  # (batch, c, r): block p is column-major r x c with ld = r
+        batch, c, r = (int(x) for x in SM.shape)
+        SM = SM.contiguous()
+        G = torch.empty((batch, c, c), dtype=torch.float64, device=SM.device)
+        check(lib.srht_gram(r, c, batch, SM.data_ptr(), r, r * c, G.data_ptr(), c, c * c,
+                            _stream_ptr(SM.device)), "srht_gram")
+        return G
+    SM = colmajor(SM)
+    r, c = int(SM.shape[0]), int(SM.shape[1])
+    ld = int(SM.stride(1)) if c > 1 else max(r, 1)
+    G = torch.empty((c, c), dtype=torch.float64, device=SM.device)
+    check(lib.srht_gram(r, c, 1, SM.data_ptr(), ld, ld * c, G.data_ptr(), c, c * c, _stream_ptr(SM.device)),
+          "srht_gram")
+    return G
+
+
+def nnls_gram(G):
+    """Lawson-Hanson NNLS on the Gram form (srht_nnls_gram): x = argmin_{x>=0} x^T Q x - 2 q^T x.
+
+    G: float64 CUDA tensor (c, c) or (batch, c, c) from :func:`gram` of [SA | Sb] (c = d + 1).
+    Returns (x, iters): x float64 (d,) or (batch, d); iters int32 (outer iterations, or a
+    negative failure code per problem, see the header).
+    """
+    torch = _torch()
+    lib = _lib.load()
+    if not G.is_cuda or G.dtype != torch.float64:
+        raise ValueError("G must be a float64 CUDA tensor")
+    single = G.dim() == 2
+    Gb = (G.unsqueeze(0) if single else G).contiguous()
+    batch, c = int(Gb.shape[0]), int(Gb.shape[1])
+    d = c - 1
+    x = torch.empty((batch, d), dtype=torch.float64, device=G.device)
+    iters = torch.empty((batch,), dtype=torch.int32, device=G.device)
+    wsb = int(lib.srht_nnls_workspace_bytes(d, batch))
+    ws = torch.empty((max(wsb, 8) // 8,), dtype=torch.float64, device=G.device)
+    check(lib.srht_nnls_gram(d, batch, Gb.data_ptr(), c, c * c, x.data_ptr(), d, iters.data_ptr(),
+                             ws.data_ptr(), wsb, _stream_ptr(G.device)), "srht_nnls_gram")
+    return (x[0], iters[0]) if single else (x, iters)

@@ -51,6 +51,9 @@ SIGNATURES = [
     ("srht_sketch_batched", ctypes.c_int, [_P, _MP, _P, _P, ctypes.c_size_t, _P]),
     ("srht_sketch_columns_host", ctypes.c_int, [_P, _MP, _P, _I64]),
     ("srht_row_shard_rows", ctypes.c_int64, [_P]),
+    ("srht_gram", ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P]),
+    ("srht_nnls_workspace_bytes", ctypes.c_size_t, [_I64, _I64]),
+    ("srht_nnls_gram", ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P]),
     ("srht_sketch_rows_partial", ctypes.c_int, [_P, _MP, _I64, _P, _I64, _P, ctypes.c_size_t, _P]),
     ("srht_status_str", ctypes.c_char_p, [ctypes.c_int]),
     ("srht_gen_uniform", ctypes.c_int, [_U64, _U64, _I64, _I64, _P, _I64, _P]),

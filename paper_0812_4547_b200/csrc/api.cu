@@ -550,6 +550,33 @@ srht_status srht_sketch_rows_partial(const srht_plan* P, const srht_matrix* M, i
   return run(P, sp, ws, ws_bytes, stream, row0, M->rows);
 }
 
+srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
+                      double* G, int64_t ldg, int64_t stride_g, void* stream) {
+  if (r < 1 || c < 1 || batch < 1 || !SM || !G || ldsm < r || ldg < c) return SRHT_EINVAL;
+  if (batch > 1 && (stride_sm < ldsm * c || stride_g < ldg * c)) return SRHT_EINVAL;
+  return srht::launch_gram(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
+size_t srht_nnls_workspace_bytes(int64_t d, int64_t batch) {
+  if (d < 1 || batch < 1 || srht::nnls_factor_in_smem(d)) return 0;
+  return (size_t)batch * (size_t)d * (size_t)d * sizeof(double);
+}
+
+srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
+                           int64_t stride_x, int32_t* iters, void* workspace, size_t workspace_bytes, void* stream) {
+  if (d < 1 || batch < 1 || !G || !x || ldg < d + 1 || d > 4096) return SRHT_EINVAL;
+  if (batch > 1 && (stride_g < ldg * (d + 1) || stride_x < d)) return SRHT_EINVAL;
+  const size_t need = srht_nnls_workspace_bytes(d, batch);
+  if (need && (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 7))) return SRHT_EINVAL;
+  return srht::launch_nnls_gram(d, batch, G, ldg, stride_g, x, stride_x, iters, static_cast<double*>(workspace),
+                                static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
 // Undeclared test hook: copy the kernel-v2 consumer slot layout to the host.
 int srht_debug_copy_ws_layout(const srht_plan* P, uint32_t* meta, int32_t* perm, int* rpt2) {
   if (!P || !P->ws_ok) return 1;

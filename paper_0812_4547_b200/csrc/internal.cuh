@@ -134,6 +134,15 @@ cudaError_t launch_sketch_tma(const srht_plan* P, const V3Params& vp, cudaStream
 int v3_mid(int x);  // kernel-v3 z layout (host side, for the slot layout)
 extern int g_kernel_force;  // 0 auto, 2 = kernel v2 instead of v3 (srht_debug_set_kernel)
 extern int g_last_kernel;   // 1/2/3: tile kernel of the last srht_sketch* call (bench labels)
+// Gram matrices of sketches (gram.cu): G_p = SM_p^T SM_p in FP64.
+cudaError_t launch_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
+                        double* G, int64_t ldg, int64_t stride_g, cudaStream_t stream);
+
+// Batched Lawson-Hanson NNLS on the Gram form (nnls.cu).
+bool nnls_factor_in_smem(int64_t d);
+cudaError_t launch_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
+                             int64_t stride_x, int32_t* iters, double* ws, cudaStream_t stream);
+
 // Fixed-order slab reduction shared by every kernel.
 cudaError_t launch_reduce(const SketchParams& sp, int slab_shift, cudaStream_t stream);
 

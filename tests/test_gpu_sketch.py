@@ -372,3 +372,100 @@ def test_row_shard_invalid_arguments(lib):
         plan.sketch_rows_partial(M[0:g + 3], 0)             # ends inside a granule, not at n
     P = plan.sketch_rows_partial(M[g:], g)                  # ends at n: fine
     assert P.dtype == torch.float64 and P.shape == (r, 2)
+
+
+# ---- Gram matrices of sketches (the QP form of P:570-590) ----
+
+def test_gram_matches_oracle(lib):
+    import torch
+    from oracle import gram as og
+    rng = np.random.default_rng(31)
+    for r, c in [(1000, 37), (8192, 65), (31, 1), (16384, 128)]:
+        SM = rng.standard_normal((r, c)).astype(np.float32)
+        G = lib.gram(to_dev(SM)).cpu().numpy()
+        ref = og.gram(SM.astype(np.float64))
+        absdot = np.abs(SM.astype(np.float64)).T @ np.abs(SM.astype(np.float64))
+        assert np.all(np.abs(G - ref) <= 1e-12 * absdot + 1e-300)
+        assert np.array_equal(G, G.T)
+
+
+def test_gram_of_batched_sketches(lib):
+    import torch
+    from oracle import gram as og
+    batch, n, c, r = 9, 3000, 5, 256
+    M = np.random.default_rng(32).random((n, batch * c), dtype=np.float32)
+    plan = lib.Plan(n, c - 1, r, 17, batch=batch)
+    SMb = plan.sketch_batched(to_dev(M))          # (batch, c, r)
+    G = lib.gram(SMb).cpu().numpy()
+    SMh = SMb.cpu().numpy().astype(np.float64)
+    for p in range(batch):
+        ref = og.gram(SMh[p].T)
+        absdot = np.abs(SMh[p]) @ np.abs(SMh[p]).T
+        assert np.all(np.abs(G[p] - ref) <= 1e-12 * absdot + 1e-300)
+
+
+# ---- NNLS on the Gram form: Algorithm 1 step 5 on the GPU ----
+
+def _nnls_problem(rng, r, d, zeros):
+    SA = rng.standard_normal((r, d)).astype(np.float32)
+    xs = rng.random(d)
+    xs[rng.choice(d, zeros, replace=False)] = 0.0
+    Sb = (SA.astype(np.float64) @ xs + 0.1 * rng.standard_normal(r)).astype(np.float32)
+    return SA, Sb
+
+
+@pytest.mark.parametrize("r,d,zeros", [(64, 8, 4), (512, 50, 20), (2048, 100, 50), (4096, 200, 100)])
+def test_nnls_gram_matches_lawson_hanson(lib, r, d, zeros):
+    from oracle import nnls
+    rng = np.random.default_rng(d)
+    SA, Sb = _nnls_problem(rng, r, d, zeros)
+    G = lib.gram(to_dev(np.column_stack([SA, Sb])))
+    x, it = lib.nnls_gram(G)
+    x = x.cpu().numpy()
+    assert int(it) > 0
+    A64, b64 = SA.astype(np.float64), Sb.astype(np.float64)
+    xr = nnls.lawson_hanson(A64, b64)[0]
+    f = lambda v: float(np.sum((A64 @ v - b64) ** 2))
+    assert abs(f(x) - f(xr)) <= 1e-10 * f(xr)
+    assert np.all(x >= 0)
+    assert np.array_equal(x > 0, xr > 0)  # same support
+    assert np.max(np.abs(x - xr)) <= 1e-8 * max(1.0, np.max(np.abs(xr)))
+    assert nnls.kkt_violation(A64, b64, x) <= 1e-9
+    if d <= 10:
+        xb = nnls.nnls_bruteforce(A64, b64)
+        assert abs(f(x) - f(xb)) <= 1e-10 * f(xb)
+
+
+def test_randomized_nnls_end_to_end_on_gpu(lib):
+    # Algorithm 1 on the GPU: sketch (config-1 shape) -> Gram -> Lawson-Hanson, against the
+    # oracle pipeline (oracle sketch, oracle LH) through R(x~) on the original data.
+    from oracle import nnls, srht as osr
+    n, d, r, seed = 4096, 16, 256, 0
+    M, _ = workloads.dense_host(n, d, seed=seed)
+    plan = lib.Plan(n, d, r, seed)
+    SM = plan.sketch_columns(to_dev(M))
+    x, it = lib.nnls_gram(lib.gram(SM))
+    x = x.cpu().numpy()
+    A, b = M[:, :d].astype(np.float64), M[:, d].astype(np.float64)
+    ref = osr.sketch(M.astype(np.float64), seed, r)
+    xo = nnls.solve_sketched(ref[:, :d], ref[:, d])
+    Rg, Ro = nnls.residual_norm(A, x, b), nnls.residual_norm(A, xo, b)
+    assert abs(Rg - Ro) / Ro <= 1e-6
+
+
+def test_batched_gram_nnls_config2_shape(lib):
+    # config-2 shape class: many independent sparse problems, sketch -> Gram -> NNLS batched
+    from oracle import nnls
+    w = workloads.config2_host(workloads.SEED, batch=40)
+    n, d, batch, r = w["n"], w["d"], w["batch"], w["r"]
+    c = d + 1
+    plan = lib.Plan(n, d, r, workloads.SEED, batch=batch)
+    SMb = plan.sketch_batched(_csc_dev(w["colptr"], w["rowidx"], w["vals"], (n, batch * c)))
+    x, it = lib.nnls_gram(lib.gram(SMb))
+    x, it, SMh = x.cpu().numpy(), it.cpu().numpy(), SMb.cpu().numpy().astype(np.float64)
+    assert np.all(it > 0)
+    for p in range(0, batch, 7):
+        SA, Sb = SMh[p, :d].T, SMh[p, d]
+        xr = nnls.lawson_hanson(SA, Sb)[0]
+        f = lambda v: float(np.sum((SA @ v - Sb) ** 2))
+        assert abs(f(x[p]) - f(xr)) <= 1e-10 * f(xr)
