@@ -101,11 +101,20 @@ enum {
    * FP32 rounding floor); it is several times slower than the
    * default FP32 path, which it does not replace.  Workspace: FP64 partials
    * (srht_workspace_bytes accounts for it).                                  */
-  SRHT_PLAN_ACCUM_FP64 = 1
+  SRHT_PLAN_ACCUM_FP64 = 1,
+  /* Algorithm 1 step 2 read verbatim: every row of S H_N is
+   * kept independently with probability r/N -- row i iff u_i < floor(2^64 r/N)
+   * (u_i = word i of stream (seed, 1), the same keys as the exact-r
+   * selection) -- so the kept count r' is random with mean r.  srht_plan_info
+   * reports r' (the sketches have r' rows); the scale stays r^{-1/2} for the
+   * requested r.  Single-problem plans only (batch = 1); r' = 0 is
+   * SRHT_EUNSUPPORTED.                                                      */
+  SRHT_PLAN_BERNOULLI = 2
 };
 
-/* srht_plan_create_batched with flags (0 or SRHT_PLAN_ACCUM_FP64); any other
- * bit is SRHT_EINVAL.  Same requirements and errors otherwise.               */
+/* srht_plan_create_batched with flags (an OR of SRHT_PLAN_ACCUM_FP64 and
+ * SRHT_PLAN_BERNOULLI); any other bit is SRHT_EINVAL.  Same requirements and
+ * errors otherwise.                                                          */
 srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed,
                                 int64_t batch, uint32_t flags,
                                 srht_plan** out);

@@ -68,6 +68,25 @@ def plan_samples(seed, p, N, r):
     return np.sort(order[:r]).astype(np.int64)
 
 
+def bernoulli_threshold(N, r):
+    """Keep threshold for Algorithm 1 step 2 read verbatim:
+    row i is kept iff u_i < T with T = floor(2^64 r / N), i.e. with probability r/N for a
+    uniform 64-bit u_i (exactly r/N when N is a power of two)."""
+    return (int(r) << 64) // int(N)
+
+
+def plan_samples_bernoulli(seed, p, N, r):
+    """Kept rows under independent Bernoulli(r/N) keeps (Algorithm 1 step 2 as written):
+    {i < N : u_i < T}, ascending; the count is random with mean r (reading R1, variant)."""
+    if not (1 <= r <= N):
+        raise ValueError("need 1 <= r <= N")
+    u = stream_words(seed, 2 * p + 1, N)
+    T = bernoulli_threshold(N, r)
+    if T >= 1 << 64:
+        return np.arange(N, dtype=np.int64)
+    return np.flatnonzero(u < np.uint64(T)).astype(np.int64)
+
+
 # ----------------------------------------------------------------------------
 # Hadamard-Walsh transform (Section 2).
 # ----------------------------------------------------------------------------
@@ -114,12 +133,14 @@ def hadamard(x):
 # The sketch (Algorithm 1 step 5 inputs).
 # ----------------------------------------------------------------------------
 
-def sketch(M, seed, r, p=0, n=None):
+def sketch(M, seed, r, p=0, n=None, sampling="exact"):
     """H~ D M for M = [A | b] (n x c), float64 result of shape (r, c).
 
     Steps, in the paper's order: pad M with zero rows to N; D M
     (step 4); normalized H_N; keep rows K of S H_N with scale
-    sqrt(N/r) (steps 2-3, reading R2).
+    sqrt(N/r) (steps 2-3, reading R2).  sampling="bernoulli" keeps each row with
+    probability r/N (plan_samples_bernoulli; the result then has that random
+    number of rows, each still scaled by sqrt(N/r)).
     """
     M = np.asarray(M, dtype=np.float64)
     if M.ndim == 1:
@@ -127,7 +148,7 @@ def sketch(M, seed, r, p=0, n=None):
     n = M.shape[0] if n is None else int(n)
     N = padded_size(n)
     sigma = plan_signs(seed, p, N)
-    K = plan_samples(seed, p, N, r)
+    K = plan_samples_bernoulli(seed, p, N, r) if sampling == "bernoulli" else plan_samples(seed, p, N, r)
     Mpad = np.zeros((N, M.shape[1]), dtype=np.float64)
     Mpad[: M.shape[0]] = M
     DM = sigma[:, None] * Mpad

@@ -102,12 +102,17 @@ class Plan:
     Philox streams (R4); problem p uses streams (seed, 2p), (seed, 2p+1).
     """
 
-    def __init__(self, n, d, r, seed=0, batch=1, accum="fp32"):
+    def __init__(self, n, d, r, seed=0, batch=1, accum="fp32", sampling="exact"):
         if accum not in ("fp32", "fp64"):
             raise ValueError("accum must be 'fp32' or 'fp64'")
+        if sampling not in ("exact", "bernoulli"):
+            raise ValueError("sampling must be 'exact' or 'bernoulli'")
         self._lib = _lib.load()
         self._h = ctypes.c_void_p()
-        flags = _lib.SRHT_PLAN_ACCUM_FP64 if accum == "fp64" else 0
+        flags = (_lib.SRHT_PLAN_ACCUM_FP64 if accum == "fp64" else 0) | \
+                (_lib.SRHT_PLAN_BERNOULLI if sampling == "bernoulli" else 0)
+        self.sampling = sampling
+        self.r_target = int(r)
         check(self._lib.srht_plan_create_ex(int(n), int(d), int(r), ctypes.c_uint64(int(seed) & (2**64 - 1)),
                                             int(batch), flags, ctypes.byref(self._h)), "srht_plan_create_ex")
         self.accum = accum

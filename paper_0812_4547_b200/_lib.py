@@ -10,6 +10,7 @@ SRHT_DENSE = 0
 SRHT_CSC = 1
 
 SRHT_PLAN_ACCUM_FP64 = 1
+SRHT_PLAN_BERNOULLI = 2
 
 SRHT_OK = 0
 SRHT_EINVAL = 1

@@ -165,7 +165,7 @@ srht::SketchParams base_params(const srht_plan* P) {
   sp.S_act = P->S_act;
   sp.groups = P->groups;
   sp.scale = P->scale;
-  sp.scale_f64 = 1.0 / std::sqrt((double)P->r);
+  sp.scale_f64 = 1.0 / std::sqrt((double)P->r_target);
   return sp;
 }
 
@@ -312,7 +312,8 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
   if (!out) return SRHT_EINVAL;
   *out = nullptr;
   if (n < 1 || d < 0 || r < 1 || batch < 1 || batch > 65535) return SRHT_EINVAL;
-  if (flags & ~(uint32_t)SRHT_PLAN_ACCUM_FP64) return SRHT_EINVAL;
+  if (flags & ~(uint32_t)(SRHT_PLAN_ACCUM_FP64 | SRHT_PLAN_BERNOULLI)) return SRHT_EINVAL;
+  if ((flags & SRHT_PLAN_BERNOULLI) && batch != 1) return SRHT_EINVAL;
   int64_t N = 2;
   while (N < n) N *= 2;
   if (r > N) return SRHT_EINVAL;
@@ -328,6 +329,34 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
   P->batch = batch;
   P->seed = seed;
   P->flags = flags;
+  P->r_target = r;
+  if (flags & SRHT_PLAN_BERNOULLI) {
+    // Algorithm 1 step 2 verbatim: row i kept iff u_i < T = floor(2^64 r / N) (prob. r/N).
+    // The kept rows are then exactly the r' smallest keys, so the exact-r selection below
+    // builds them with r = r' (the count is random; the scale stays r^{-1/2}).
+    int64_t kept = N;
+    if (r < N) {
+      int lg = 0;
+      while ((int64_t(1) << lg) < N) ++lg;
+      const uint64_t T = (uint64_t)r << (64 - lg);  // N = 2^lg, r < N
+      cudaStream_t st0;
+      if (cudaStreamCreateWithFlags(&st0, cudaStreamNonBlocking) != cudaSuccess) {
+        delete P;
+        return SRHT_ECUDA;
+      }
+      const cudaError_t ce = srht::count_keys_below(seed, N, T, &kept, st0);
+      cudaStreamDestroy(st0);
+      if (ce != cudaSuccess) {
+        delete P;
+        return SRHT_ECUDA;
+      }
+    }
+    if (kept < 1) {
+      delete P;
+      return SRHT_EUNSUPPORTED;  // no row kept (probability (1 - r/N)^N)
+    }
+    P->r = r = kept;
+  }
   // Geometry (depends on n and r only).  Tile B ~ r (so ~1 sampled entry per
   // tile row, Ailon-Liberty balance), clamped to [2^10, 2^14]; slabs of ~2^20 rows.
   int lb = ceil_log2(r);
@@ -353,7 +382,7 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
   P->rpt = per <= 4 ? 4 : per <= 8 ? 8 : per <= 16 ? 16 : 32;
   P->groups = (r + (int64_t)P->rpt * P->threads - 1) / ((int64_t)P->rpt * P->threads);
   P->words64 = P->N_eff / 64;
-  P->scale = (float)(1.0 / std::sqrt((double)r));
+  P->scale = (float)(1.0 / std::sqrt((double)P->r_target));
   if (cudaGetDevice(&P->device) != cudaSuccess) {
     delete P;
     return SRHT_ECUDA;

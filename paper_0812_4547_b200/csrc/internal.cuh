@@ -8,7 +8,9 @@
 struct srht_plan {
   int64_t n, d, r, N, batch;
   uint64_t seed;
-  uint32_t flags;   // SRHT_PLAN_ACCUM_FP64: every sketch runs the FP64-accumulation kernel
+  uint32_t flags;   // SRHT_PLAN_ACCUM_FP64: every sketch runs the FP64-accumulation kernel;
+                    // SRHT_PLAN_BERNOULLI: r is the random kept count, r_target the requested r
+  int64_t r_target; // requested r (the scale is r_target^{-1/2})
   // Tile / slab geometry: depends on (n, r) only.
   int log_b;        // tile bits; B = 2^log_b rows per sub-block
   int64_t B;
@@ -45,6 +47,7 @@ namespace srht {
 
 // Plan builder (plan.cu): fills d_signs and d_K; synchronous on `stream`.
 cudaError_t build_plan_device(srht_plan* P, cudaStream_t stream);
+cudaError_t count_keys_below(uint64_t seed, int64_t N, uint64_t T, int64_t* count, cudaStream_t stream);
 cudaError_t build_ws_signs(const uint64_t* signs, int64_t n_tiles, uint4* out, cudaStream_t stream);
 cudaError_t build_v3_signs(const uint64_t* signs, int64_t n_tiles, uint4* out, cudaStream_t stream);
 

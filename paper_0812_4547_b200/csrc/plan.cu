@@ -203,6 +203,34 @@ cudaError_t dev_alloc(T** p, size_t count) {
 
 }  // namespace
 
+// Number of keys u_i < T (i < N) of problem 0's sampling stream: the kept count of the
+// Bernoulli(r/N) plan (T = floor(2^64 r / N)), computed with the selection's count pass.
+cudaError_t count_keys_below(uint64_t seed, int64_t N, uint64_t T, int64_t* count, cudaStream_t stream) {
+  const int64_t chunks = (N + kChunk - 1) / kChunk;
+  uint64_t* thr = nullptr;
+  int32_t *n_less = nullptr, *n_eq = nullptr;
+  cudaError_t err;
+  do {
+    if ((err = dev_alloc(&thr, 1)) != cudaSuccess) break;
+    if ((err = dev_alloc(&n_less, chunks)) != cudaSuccess) break;
+    if ((err = dev_alloc(&n_eq, chunks)) != cudaSuccess) break;
+    if ((err = cudaMemcpyAsync(thr, &T, sizeof(T), cudaMemcpyHostToDevice, stream)) != cudaSuccess) break;
+    k_count<<<dim3((unsigned)chunks, 1u), kChunkThreads, 0, stream>>>(seed, N, chunks, thr, n_less, n_eq);
+    if ((err = cudaGetLastError()) != cudaSuccess) break;
+    int32_t* h = new int32_t[chunks];
+    err = cudaMemcpyAsync(h, n_less, chunks * sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+    int64_t tot = 0;
+    for (int64_t c = 0; c < chunks; ++c) tot += h[c];
+    delete[] h;
+    *count = tot;
+  } while (0);
+  cudaFree(thr);
+  cudaFree(n_less);
+  cudaFree(n_eq);
+  return err;
+}
+
 cudaError_t build_plan_device(srht_plan* P, cudaStream_t stream) {
   cudaError_t err = cudaSuccess;
   const int64_t batch = P->batch, N = P->N;

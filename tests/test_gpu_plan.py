@@ -47,3 +47,16 @@ def test_invalid_arguments(srht):
         with pytest.raises(srht.SrhtError) as ei:
             srht.Plan(*args)
         assert ei.value.status == SRHT_EINVAL
+
+
+# ---- Bernoulli keeps (Algorithm 1 step 2 verbatim) ----
+
+@pytest.mark.parametrize("n,r,seed", [(4096, 256, 0), (100000, 3000, 5), (1 << 20, 8192, 9), (1 << 14, 1 << 14, 2), (37, 5, 3)])
+def test_bernoulli_plan_bit_exact(srht, n, r, seed):
+    from oracle import srht as osr
+    plan = srht.Plan(n, 3, r, seed, sampling="bernoulli")
+    N = osr.padded_size(n)
+    K = osr.plan_samples_bernoulli(seed, 0, N, r)
+    assert plan.r == len(K) and plan.r_target == r
+    assert np.array_equal(plan.indices().astype(np.int64), K)
+    assert np.array_equal(plan.sign_words(), osr.sign_words(seed, 0, N))

@@ -469,3 +469,16 @@ def test_batched_gram_nnls_config2_shape(lib):
         xr = nnls.lawson_hanson(SA, Sb)[0]
         f = lambda v: float(np.sum((SA @ v - Sb) ** 2))
         assert abs(f(x[p]) - f(xr)) <= 1e-10 * f(xr)
+
+
+# ---- Bernoulli keeps: sketches with the random kept count ----
+
+@pytest.mark.parametrize("n,c,r,seed", [(4096, 5, 256, 0), (1 << 20, 3, 8192, 4), (300000, 2, 2000, 7)])
+def test_bernoulli_sketch_parity(lib, n, c, r, seed):
+    from oracle import srht as osr
+    M = np.random.default_rng(seed).standard_normal((n, c)).astype(np.float32)
+    plan = lib.Plan(n, c - 1, r, seed, sampling="bernoulli")
+    SM = plan.sketch_columns(to_dev(M), workspace=plan.workspace(c)).cpu().numpy()
+    ref = osr.sketch(M.astype(np.float64), seed, r, sampling="bernoulli")
+    assert SM.shape == ref.shape == (plan.r, c)
+    check_close(SM, ref, M)

@@ -71,3 +71,47 @@ def test_problems_have_independent_plans():
     a = srht.plan_samples(0, 0, 1024, 64)
     b = srht.plan_samples(0, 1, 1024, 64)
     assert not np.array_equal(a, b)
+
+
+# ---- Bernoulli keeps (Algorithm 1 step 2 verbatim) ----
+
+def test_bernoulli_threshold_exact():
+    # T = floor(2^64 r / N) as an exact integer: for N = 2^L it is r * 2^(64 - L)
+    for L, r in [(4, 1), (10, 37), (20, 8192), (26, 16384)]:
+        N = 1 << L
+        assert srht.bernoulli_threshold(N, r) == r * (1 << (64 - L))
+    assert srht.bernoulli_threshold(8, 8) == 1 << 64  # r = N keeps everything
+
+
+def test_bernoulli_keeps_are_the_threshold_set():
+    # brute force from the raw stream words: kept iff u_i < T, ascending
+    for seed, N, r in [(1, 64, 9), (2, 256, 100), (3, 16, 16)]:
+        u = [philox.stream_word_py(seed, 1, i) for i in range(N)]  # KAT-pinned pure-Python Philox
+        T = (r << 64) // N
+        expect = [i for i in range(N) if u[i] < T]
+        assert list(srht.plan_samples_bernoulli(seed, 0, N, r)) == expect
+
+
+def test_bernoulli_inclusion_frequency_and_count():
+    # each row kept w.p. r/N: per-index frequency and mean count over seeds (5 sigma)
+    N, r, seeds = 256, 32, 400
+    hits = np.zeros(N)
+    counts = []
+    for s in range(seeds):
+        K = srht.plan_samples_bernoulli(s, 0, N, r)
+        hits[K] += 1
+        counts.append(len(K))
+    pr = r / N
+    sd = math.sqrt(pr * (1 - pr) / seeds)
+    assert np.all(np.abs(hits / seeds - pr) <= 5 * sd + 1e-12)
+    sd_mean = math.sqrt(N * pr * (1 - pr) / seeds)
+    assert abs(np.mean(counts) - r) <= 5 * sd_mean
+
+
+def test_bernoulli_sketch_is_unbiased_in_norm():
+    # E ||S H D x||^2 = ||x||^2 with the sqrt(N/r) scale of P:298 (Monte Carlo, 4 sigma)
+    n, r = 64, 16
+    x = np.random.default_rng(0).standard_normal(n)
+    vals = [float(np.sum(srht.sketch(x, s, r, sampling="bernoulli") ** 2)) for s in range(600)]
+    m, sd = np.mean(vals), np.std(vals) / math.sqrt(len(vals))
+    assert abs(m - float(x @ x)) <= 4 * sd
