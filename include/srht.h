@@ -216,6 +216,25 @@ srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G,
                            int64_t stride_x, int32_t* iters, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* ---- Algorithm 2, SubspaceSampling ----
+ * Row i of Phi (n x d, FP32 column-major, ldphi >= n) is kept with probability
+ * q_i = min(1, r p_i) (p: n FP64 probabilities) and scaled by 1/sqrt(q_i): kept
+ * iff q_i >= 1 or u_i < floor(q_i 2^64), u_i = word i of the Philox stream
+ * (seed, 1) -- the coins of SRHT_PLAN_BERNOULLI, so p_i = 1/N applied to
+ * H_N D [M; 0] / sqrt(N) is the Bernoulli SRHT sketch.
+ * srht_subspace_sample_count: the number of kept rows into *kept (host;
+ * synchronous on `stream`).  srht_subspace_sample: kept row indices, ascending,
+ * into K (device int32, capacity cap) and the scaled rows into out (cap x d,
+ * ldout >= cap); rows beyond cap are dropped.  Temporaries are allocated
+ * stream-ordered (cudaMallocAsync).                                          */
+srht_status srht_subspace_sample_count(int64_t n, int64_t r, uint64_t seed,
+                                       const double* p, int64_t* kept,
+                                       void* stream);
+srht_status srht_subspace_sample(int64_t n, int64_t d, int64_t r, uint64_t seed,
+                                 const double* p, const float* Phi,
+                                 int64_t ldphi, int32_t* K, float* out,
+                                 int64_t ldout, int64_t cap, void* stream);
+
 /* Same as srht_sketch_columns, but M's values, column pointers, row indices
  * and SM are HOST buffers (pinned or pageable).  Host->device copies, the
  * sketch and the device->host copy run inside the call, pipelined over column

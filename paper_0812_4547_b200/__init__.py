@@ -22,7 +22,8 @@ import numpy as np
 from . import _lib
 from ._lib import SRHT_CSC, SRHT_DENSE, SrhtMatrix, SrhtError, check
 
-__all__ = ["Plan", "CSC", "SrhtError", "colmajor", "gen_uniform", "gram", "nnls_gram", "padded_size", "library"]
+__all__ = ["Plan", "CSC", "SrhtError", "colmajor", "gen_uniform", "gram", "nnls_gram", "padded_size", "library",
+           "subspace_sampling"]
 
 CSC = namedtuple("CSC", ["colptr", "rowidx", "vals", "shape"])
 CSC.__doc__ = "Compressed sparse columns: int64 colptr[c+1], int32 rowidx[nnz] (sorted per column), float32 vals."
@@ -333,3 +334,29 @@ def nnls_gram(G):
     check(lib.srht_nnls_gram(d, batch, Gb.data_ptr(), c, c * c, x.data_ptr(), d, iters.data_ptr(),
                              ws.data_ptr(), wsb, _stream_ptr(G.device)), "srht_nnls_gram")
     return (x[0], iters[0]) if single else (x, iters)
+
+
+def subspace_sampling(Phi, r, p, seed=0):
+    """Algorithm 2, SubspaceSampling (srht_subspace_sample): (K, Phi~) with K the kept row
+    indices (int32, ascending) and Phi~ the kept rows of Phi scaled by 1/sqrt(min(1, r p_i)).
+
+    Phi: float32 CUDA tensor (n, d) (column-major used as is, else copied); p: float64 CUDA
+    tensor (n,) of probabilities.
+    """
+    torch = _torch()
+    lib = _lib.load()
+    Phi = colmajor(Phi)
+    n, d = int(Phi.shape[0]), int(Phi.shape[1])
+    p = p.to(torch.float64).contiguous()
+    st = _stream_ptr(Phi.device)
+    kept = ctypes.c_int64()
+    check(lib.srht_subspace_sample_count(n, int(r), ctypes.c_uint64(int(seed) & (2**64 - 1)), p.data_ptr(),
+                                         ctypes.byref(kept), st), "srht_subspace_sample_count")
+    k = int(kept.value)
+    K = torch.empty((max(k, 1),), dtype=torch.int32, device=Phi.device)
+    out = torch.empty((d, max(k, 1)), dtype=torch.float32, device=Phi.device).t()
+    ld = int(Phi.stride(1)) if d > 1 else max(n, 1)
+    check(lib.srht_subspace_sample(n, d, int(r), ctypes.c_uint64(int(seed) & (2**64 - 1)), p.data_ptr(),
+                                   Phi.data_ptr(), ld, K.data_ptr(), out.data_ptr(), max(k, 1), k, st),
+          "srht_subspace_sample")
+    return K[:k], out[:k]

@@ -54,6 +54,8 @@ SIGNATURES = [
     ("srht_row_shard_rows", ctypes.c_int64, [_P]),
     ("srht_gram", ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P]),
     ("srht_nnls_workspace_bytes", ctypes.c_size_t, [_I64, _I64]),
+    ("srht_subspace_sample_count", ctypes.c_int, [_I64, _I64, _U64, _P, ctypes.POINTER(_I64), _P]),
+    ("srht_subspace_sample", ctypes.c_int, [_I64, _I64, _I64, _U64, _P, _P, _I64, _P, _P, _I64, _I64, _P]),
     ("srht_nnls_gram", ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P]),
     ("srht_sketch_rows_partial", ctypes.c_int, [_P, _MP, _I64, _P, _I64, _P, ctypes.c_size_t, _P]),
     ("srht_status_str", ctypes.c_char_p, [ctypes.c_int]),

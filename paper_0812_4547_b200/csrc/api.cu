@@ -606,6 +606,25 @@ srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ld
              : SRHT_ECUDA;
 }
 
+srht_status srht_subspace_sample_count(int64_t n, int64_t r, uint64_t seed, const double* p, int64_t* kept,
+                                       void* stream) {
+  if (n < 1 || r < 1 || !p || !kept) return SRHT_EINVAL;
+  return srht::launch_subspace(n, 0, r, seed, p, nullptr, 1, nullptr, nullptr, 1, 0, kept,
+                               static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
+srht_status srht_subspace_sample(int64_t n, int64_t d, int64_t r, uint64_t seed, const double* p, const float* Phi,
+                                 int64_t ldphi, int32_t* K, float* out, int64_t ldout, int64_t cap, void* stream) {
+  if (n < 1 || d < 0 || r < 1 || !p || !K || cap < 0 || (d > 0 && (!Phi || !out || ldphi < n || ldout < cap)))
+    return SRHT_EINVAL;
+  return srht::launch_subspace(n, d, r, seed, p, Phi, ldphi, K, out, ldout, cap, nullptr,
+                               static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
 // Undeclared test hook: copy the kernel-v2 consumer slot layout to the host.
 int srht_debug_copy_ws_layout(const srht_plan* P, uint32_t* meta, int32_t* perm, int* rpt2) {
   if (!P || !P->ws_ok) return 1;

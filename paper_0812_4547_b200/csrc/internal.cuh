@@ -146,6 +146,11 @@ bool nnls_factor_in_smem(int64_t d);
 cudaError_t launch_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
                              int64_t stride_x, int32_t* iters, double* ws, cudaStream_t stream);
 
+// Algorithm 2 SubspaceSampling (subspace.cu).
+cudaError_t launch_subspace(int64_t n, int64_t d, int64_t r, uint64_t seed, const double* p, const float* Phi,
+                            int64_t ldphi, int32_t* K, float* out, int64_t ldout, int64_t cap, int64_t* kept,
+                            cudaStream_t stream);
+
 // Fixed-order slab reduction shared by every kernel.
 cudaError_t launch_reduce(const SketchParams& sp, int slab_shift, cudaStream_t stream);
 

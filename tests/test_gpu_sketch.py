@@ -482,3 +482,35 @@ def test_bernoulli_sketch_parity(lib, n, c, r, seed):
     ref = osr.sketch(M.astype(np.float64), seed, r, sampling="bernoulli")
     assert SM.shape == ref.shape == (plan.r, c)
     check_close(SM, ref, M)
+
+
+# ---- Algorithm 2, SubspaceSampling ----
+
+def test_subspace_sampling_matches_oracle(lib):
+    import torch
+    from oracle import subspace
+    rng = np.random.default_rng(41)
+    for n, d, r in [(5000, 4, 300), (100000, 2, 2000), (77, 3, 100)]:
+        Phi = rng.standard_normal((n, d)).astype(np.float32)
+        p = rng.random(n) ** 2
+        p[0] = 1e3  # r p_0 >= 1: kept with scale 1
+        p /= p.sum()
+        K, rows = lib.subspace_sampling(to_dev(Phi), r, torch.from_numpy(p).cuda(), seed=n)
+        Ko, ro = subspace.subspace_sampling(Phi.astype(np.float64), r, p, n)
+        assert np.array_equal(K.cpu().numpy().astype(np.int64), Ko)   # bit-exact keep decisions
+        np.testing.assert_allclose(rows.cpu().numpy(), ro, rtol=1e-6, atol=0)  # one FP32 rounding
+
+
+def test_subspace_uniform_equals_bernoulli_srht(lib):
+    # p_i = 1/N on Phi = H_N D [M; 0] / sqrt(N) (formed by the oracle) keeps the Bernoulli plan's rows
+    import torch
+    from oracle import srht as osr
+    n, r, seed = 3000, 200, 5
+    M = np.random.default_rng(2).standard_normal((n, 2))
+    N = osr.padded_size(n)
+    Mp = np.zeros((N, 2))
+    Mp[:n] = M
+    Phi = (osr.hadamard(osr.plan_signs(seed, 0, N)[:, None] * Mp) / np.sqrt(N)).astype(np.float32)
+    K, rows = lib.subspace_sampling(to_dev(Phi), r, torch.full((N,), 1.0 / N, dtype=torch.float64).cuda(), seed=seed)
+    plan = lib.Plan(n, 1, r, seed, sampling="bernoulli")
+    assert np.array_equal(K.cpu().numpy(), plan.indices())
