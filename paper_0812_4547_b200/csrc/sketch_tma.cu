@@ -62,7 +62,9 @@ __device__ __forceinline__ float flipf(float x, uint32_t mask) { return __uint_a
 
 template <int CH>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&w)[CH]) {
-  if constexpr (CH == 8) {
+  if constexpr (CH == 2) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(taddr));
+  } else if constexpr (CH == 8) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
                  : "r"(taddr));
@@ -233,7 +235,8 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
 // Experiment variants (DBG != 0 only for srht_debug_set_trace / srht_debug_set_mode; results
 // are wrong for the knock-outs): bit 0 = clock64 at phase boundaries of CTA 0 for flat tiles
 // 16..79 (scripts/v3_trace.py); bit 1 = consumers skip the gather loads; bit 2 = producers
-// skip the butterflies; bit 3 = producers skip the shared-memory loads/stores of both rounds.
+// skip the butterflies; bit 3 = producers skip the shared-memory loads/stores of both rounds;
+// bit 4 = producers skip the whole transform (data movement only).
 #define V3_TRACE(role, k, pt)                                                            \
   if ((DBG & 1) && blockIdx.x == 0 && (k) >= 16 && (k) < 80)                             \
     P.trace[((size_t)(role) * 64 + ((k) - 16)) * 8 + (pt)] = clock64();
@@ -287,6 +290,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       if (p == 0) { V3_TRACE(g, f, 0) }
       mbar_wait(smem_u32(smem + CTRL_OFF + 8 * b), parity);
       if (p == 0) { V3_TRACE(g, f, 6) }
+      if (DBG & 16) {  // knock-out: data movement only (no transform at all)
+        bar_arrive(BAR_READY0 + b, 384);
+        cursor_next_active(P, cur);
+        cursor_next_active(P, cur);
+        f += 2;
+        continue;
+      }
       const uint4 sg = *reinterpret_cast<const uint4*>(smem + SIGN_OFF + 2048 * b + 16 * p);
       float2 v[64];
       // ---- round 1: rows x = e + 2p + 256h; quarter q = h in [16q, 16q+16) ----
@@ -395,6 +405,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
     float acc[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) acc[q] = 0.f;
+    // Gather offsets are the same for every tile, so their TMEM loads run one chunk ahead
+    // across tile boundaries too (an even number of chunks keeps the buffer parity fixed).
+    constexpr int CH = MW >= 16 ? 8 : MW / 2;  // meta words per TMEM load
+    static_assert((MW / CH) % 2 == 0, "even chunk count");
+    uint32_t w[2][CH];
+    tmem_ld<CH>(taddr, w[0]);
     int f = 0;
     for (int it = blockIdx.x; it < P.n_items32; it += gridDim.x) {
       Cursor ci;
@@ -409,13 +425,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
           const float* buf = reinterpret_cast<const float*>(smem + (size_t)b * BUF_BYTES);
           if (c == 0) { V3_TRACE(2, f, 0) }
           bar_sync(BAR_READY0 + b, 384);
-          constexpr int CH = MW < 8 ? MW : 8;  // meta words per TMEM load
-          uint32_t w[2][CH];
-          tmem_ld<CH>(taddr, w[0]);
 #pragma unroll
           for (int k = 0; k < MW; k += CH) {
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (k + CH < MW) tmem_ld<CH>(taddr + k + CH, w[((k / CH) + 1) & 1]);  // next chunk in flight
+            // next chunk in flight (after the last chunk: chunk 0 of the next tile)
+            tmem_ld<CH>(taddr + (k + CH) % MW, w[((k / CH) + 1) & 1]);
             if (k == 0 && c == 0) { V3_TRACE(2, f, 1) }
             const uint32_t* wk = w[(k / CH) & 1];
 #pragma unroll
@@ -469,6 +483,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
         acc[q] = 0.f;
       }
     }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");  // the last look-ahead load
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     bar_sync(BAR_CONS, NCONS);
     if (wc == 0) {
@@ -503,6 +518,8 @@ cudaError_t launch_rpt(const V3Params& vp, int grid, cudaStream_t stream) {
       case 10: return launch_dbg<RPT, 10>(vp, grid, stream);
       case 12: return launch_dbg<RPT, 12>(vp, grid, stream);
       case 14: return launch_dbg<RPT, 14>(vp, grid, stream);
+      case 16: return launch_dbg<RPT, 16>(vp, grid, stream);
+      case 18: return launch_dbg<RPT, 18>(vp, grid, stream);
       default: break;
     }
   }
