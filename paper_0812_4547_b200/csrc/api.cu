@@ -122,13 +122,14 @@ cudaError_t build_ws_layout(srht_plan* P, const std::vector<int32_t>& K) {
 }
 
 // Kernel v3: per consumer thread c, rpt2/2 words of two 15-bit mid-layout word
-// offsets (slot q = 2i in bits 0..14, 2i+1 in bits 17..31 of word i); perm =
-// t | k_mid << 16; masks[sh][c] bit q = bit sh of k_mid of slot (q, c).
+// offsets (slot q = 2i in bits 0..14, 2i+1 in bits 17..31 of word i); ttab, the
+// same shape: the two slots' output rows t (bits 0..15, 16..31; 0xffff = empty slot);
+// masks[sh][c] bit q = bit sh of k_mid of slot (q, c).
 cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
   const int rpt = P->rpt2, slots = rpt * 256, mw = rpt / 2;
   const std::vector<int32_t> slot_t = deal_slots(K, rpt, srht::v3_mid);
   std::vector<uint32_t> meta((size_t)256 * mw, 0u);
-  std::vector<int32_t> perm(slots, -1);
+  std::vector<uint32_t> ttab((size_t)256 * mw, 0xffffffffu);
   std::vector<uint2> masks((size_t)(P->log_j2 > 0 ? P->log_j2 : 1) * 256, make_uint2(0u, 0u));
   for (int q = 0; q < rpt; ++q)
     for (int c = 0; c < 256; ++c) {
@@ -138,7 +139,8 @@ cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
       const uint32_t off = (uint32_t)srht::v3_mid(k & ((1 << 14) - 1));
       const uint32_t kmid = (uint32_t)(k >> 14) & (uint32_t)(P->J2 - 1);
       meta[(size_t)c * mw + q / 2] |= off << (17 * (q & 1));  // lo | hi << 17
-      perm[q * 256 + c] = t | (int32_t)(kmid << 16);
+      uint32_t& tw = ttab[(size_t)c * mw + q / 2];
+      tw = (tw & ~(0xffffu << (16 * (q & 1)))) | ((uint32_t)t << (16 * (q & 1)));
       for (int sh = 0; sh < P->log_j2; ++sh)
         if ((kmid >> sh) & 1u) {
           uint2& m = masks[(size_t)sh * 256 + c];
@@ -146,7 +148,7 @@ cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
         }
     }
   cudaError_t e = upload(&P->d_meta3, meta);
-  if (e == cudaSuccess) e = upload(&P->d_perm3, perm);
+  if (e == cudaSuccess) e = upload(&P->d_ttab3, ttab);
   if (e == cudaSuccess) e = upload(&P->d_masks3, masks);
   return e;
 }
@@ -238,7 +240,7 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       vp.total_cols = rp.total_cols;
       vp.signs = P->d_signs3;
       vp.meta = P->d_meta3;
-      vp.perm = P->d_perm3;
+      vp.ttab = P->d_ttab3;
       vp.masks = P->d_masks3;
       vp.log_j = P->log_j2;
       vp.r = P->r;
@@ -437,7 +439,7 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
         cudaStreamDestroy(st2);
       }
     }
-    P->v3_ok = (e == cudaSuccess) && P->log_j2 <= srht::V3_MAX_LOGJ;
+    P->v3_ok = (e == cudaSuccess) && P->log_j2 <= srht::V3_MAX_LOGJ && P->r < 0xffff;  // 16-bit t table
   }
   if (e != cudaSuccess) {
     srht_plan_destroy(P);
@@ -465,7 +467,7 @@ srht_status srht_plan_destroy(srht_plan* P) {
   cudaFree(P->d_signs_ws);
   cudaFree(P->d_signs3);
   cudaFree(P->d_meta3);
-  cudaFree(P->d_perm3);
+  cudaFree(P->d_ttab3);
   cudaFree(P->d_masks3);
   delete P;
   return SRHT_OK;

@@ -39,7 +39,7 @@ struct srht_plan {
   bool v3_ok;
   uint4* d_signs3;    // [N/2^14][128] sign bits of rows e + 2p + 256h, bit 2h+e
   uint32_t* d_meta3;  // [256][rpt2/2]: two 16-bit mid-layout word offsets per word
-  int32_t* d_perm3;   // [rpt2][256]: t | k_mid << 16, or -1
+  uint32_t* d_ttab3;  // [256][rpt2/2]: output rows t of slots (2i, 2i+1), 16 bits each (0xffff: empty)
   uint2* d_masks3;    // [log_j2][256]: bit q = bit sh of k_mid of slot (q, c)
 };
 
@@ -120,7 +120,7 @@ struct V3Params {
   int64_t ncols0, total_cols;
   const uint4* signs;     // plan d_signs3
   const uint32_t* meta;   // plan d_meta3
-  const int32_t* perm;    // plan d_perm3
+  const uint32_t* ttab;   // plan d_ttab3
   const uint2* masks;     // plan d_masks3
   int log_j;
   int64_t r, n;

@@ -47,7 +47,20 @@ constexpr int NTHREADS = 512;
 constexpr int SIGN_OFF = NBUF * BUF_BYTES;            // per buffer: 128 threads x 16 B of D bits
 constexpr int MASK_OFF = SIGN_OFF + NBUF * 2048;
 constexpr int CTRL_OFF = MASK_OFF + V3_MAX_LOGJ * NCONS * 8;
-constexpr int SMEM_BYTES = CTRL_OFF + 256;  // mbarriers [0,24), TMEM address [32,36), slot states [64,..)
+#ifndef V3_EMPTY_MBAR
+#define V3_EMPTY_MBAR 1
+#endif
+#ifndef V3_QSPLIT
+#define V3_QSPLIT 1
+#endif
+// FULL mbarriers: NQ per buffer, one per contiguous 1/NQ of the tile (round 1 reads the
+// tile quarter by quarter, so it starts as soon as the first quarter has landed).
+constexpr int NQ = V3_QSPLIT ? 4 : 1;
+// control block: FULL mbarriers [0, 8 NQ NBUF), TMEM address [96,100), EMPTY mbarriers
+// [104,128), slot states [128,..)
+constexpr int CTRL_TMEM = 96, CTRL_EMPTY = 104, CTRL_SLOTS = 128, CTRL_BYTES = 384;
+static_assert(8 * NQ * NBUF <= CTRL_TMEM, "FULL mbarriers overflow");
+constexpr int SMEM_BYTES = CTRL_OFF + CTRL_BYTES;
 
 enum { BAR_READY0 = 1, BAR_GRP0 = 4, BAR_CONS = 6 };  // named barriers (0 = __syncthreads)
 
@@ -180,7 +193,7 @@ struct SlotState {
 #ifndef V3_L2_HINTS
 #define V3_L2_HINTS 1
 #endif
-static_assert(64 + NBUF * sizeof(SlotState) <= 256, "control block overflows");
+static_assert(CTRL_SLOTS + NBUF * sizeof(SlotState) <= CTRL_BYTES, "control block overflows");
 
 __device__ __forceinline__ void tile_src(const V3Params& P, const Cursor& c, int& tile, const float*& src, bool& full) {
   tile = c.s * P.J32 + gray(c.pp);
@@ -192,14 +205,20 @@ __device__ __forceinline__ void tile_src(const V3Params& P, const Cursor& c, int
 __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int b, unsigned char* smem) {
   Cursor c = st.cur;
   if (c.it >= P.n_items32) return;
-  const uint32_t bar = smem_u32(smem + CTRL_OFF + 8 * b);
+  const uint32_t bar = smem_u32(smem + CTRL_OFF + 8 * NQ * b);  // quarter q: bar + 8 q
   int tile;
   const float* src;
   bool full;
   tile_src(P, c, tile, src, full);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(full ? B * 4 + 2048 : 2048)
-               : "memory");
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {  // signs ride with the first part; a tail tile has no data parts
+    const int bytes = (full ? B * 4 / NQ : 0) + (q == 0 ? 2048 : 0);
+    if (bytes)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar + 8 * q), "r"(bytes) : "memory");
+    else
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar + 8 * q) : "memory");
+  }
   uint64_t keep, stream;
   if (V3_L2_HINTS) {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
@@ -216,11 +235,11 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
   if (full) {  // a tail tile is loaded by the producers themselves (guarded)
     const uint32_t dst = smem_u32(smem + (size_t)b * BUF_BYTES);
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < 4; ++k)  // 16 KB each (the bulk-copy size limit is 1 MB; 16 KB keeps parts even)
       asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], 32768, [%2], %3;" ::"r"(
-              dst + k * 32768),
-          "l"(reinterpret_cast<const char*>(src) + k * 32768), "r"(bar), "l"(stream)
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], 16384, [%2], %3;" ::"r"(
+              dst + k * 16384),
+          "l"(reinterpret_cast<const char*>(src) + k * 16384), "r"(bar + 8 * (k * NQ / 4)), "l"(stream)
           : "memory");
   }
 #pragma unroll
@@ -234,27 +253,33 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
 
 // Experiment variants (DBG != 0 only for srht_debug_set_trace / srht_debug_set_mode; results
 // are wrong for the knock-outs): bit 0 = clock64 at phase boundaries of CTA 0 for flat tiles
-// 16..79 (scripts/v3_trace.py); bit 1 = consumers skip the gather loads; bit 2 = producers
+// 0..4095 (scripts/v3_trace.py); bit 1 = consumers skip the gather loads; bit 2 = producers
 // skip the butterflies; bit 3 = producers skip the shared-memory loads/stores of both rounds;
 // bit 4 = producers skip the whole transform (data movement only).
+#define V3_TRACE_TILES 4096  // CTA 0, flat tiles 0..4095; trace buffer 3 x 4096 x 8 int64
 #define V3_TRACE(role, k, pt)                                                            \
-  if ((DBG & 1) && blockIdx.x == 0 && (k) >= 16 && (k) < 80)                             \
-    P.trace[((size_t)(role) * 64 + ((k) - 16)) * 8 + (pt)] = clock64();
+  if ((DBG & 1) && blockIdx.x == 0 && (k) < V3_TRACE_TILES)                              \
+    P.trace[((size_t)(role) * V3_TRACE_TILES + (k)) * 8 + (pt)] = clock64();
 
 template <int RPT, int DBG>
 __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constant__ V3Params P) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint2* masks_s = reinterpret_cast<uint2*>(smem + MASK_OFF);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + 32);
-  SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + 64);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + CTRL_TMEM);
+  SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + CTRL_SLOTS);
   constexpr int MW = RPT / 2;                        // packed meta words (TMEM columns) per consumer thread
-  constexpr int TCOLS = (2 * MW) < 32 ? 32 : 2 * MW; // TMEM columns allocated (two consumer warps per lane quarter)
+  // TMEM columns: gather offsets [0, 2 MW) then output rows [2 MW, 4 MW) (two consumer
+  // warps per lane quarter, MW columns each)
+  constexpr int TCOLS = (4 * MW) < 32 ? 32 : 4 * MW;
   const int tid = threadIdx.x;
 
   // ---------------- setup (all threads) ----------------
   if (tid == 0) {
-    for (int b = 0; b < NBUF; ++b)
+    for (int b = 0; b < NQ * NBUF; ++b)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(smem + CTRL_OFF + 8 * b)));
+    for (int b = 0; b < NBUF; ++b)  // EMPTY[b]: one arrival per consumer warp
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b)),
+                   "r"(NCONS / 32));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid >= 256 && tid < 288) {  // consumer warp 0 allocates TMEM
@@ -288,9 +313,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       const float* __restrict__ colp = col_ptr(P, cur.col);
       float* buf = reinterpret_cast<float*>(smem + (size_t)b * BUF_BYTES);
       if (p == 0) { V3_TRACE(g, f, 0) }
-      mbar_wait(smem_u32(smem + CTRL_OFF + 8 * b), parity);
+      const uint32_t fullb = smem_u32(smem + CTRL_OFF + 8 * NQ * b);
+      mbar_wait(fullb, parity);  // first part (and the signs)
       if (p == 0) { V3_TRACE(g, f, 6) }
       if (DBG & 16) {  // knock-out: data movement only (no transform at all)
+        for (int q = 1; q < NQ; ++q) mbar_wait(fullb + 8 * q, parity);
         bar_arrive(BAR_READY0 + b, 384);
         cursor_next_active(P, cur);
         cursor_next_active(P, cur);
@@ -303,6 +330,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       if (row0 + B > n) {
         // tail tile (not copied by TMA): the group stages it in the raw layout itself,
         // zero-filling rows >= n, then reads it back like any other tile
+        for (int q = 1; q < NQ; ++q) mbar_wait(fullb + 8 * q, parity);  // (data-less parts)
 #pragma unroll 4
         for (int h = 0; h < 64; ++h) {
           const int row = row0 + 2 * p + 256 * h;
@@ -313,6 +341,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
+        if (NQ == 4 && q > 0) mbar_wait(fullb + 8 * q, parity);
 #pragma unroll
         for (int h = 16 * q; h < 16 * q + 16; ++h)
           v[h] = (DBG & 8) ? make_float2((float)h, (float)p) : *reinterpret_cast<const float2*>(buf + 2 * p + 256 * h);
@@ -391,6 +420,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
                    "r"(m4.y), "r"(m4.z), "r"(m4.w)
                    : "memory");
     }
+    // output rows (slab epilogue) -> TMEM (once): a global load per output there would
+    // serialise behind the output stores (measured ~29 us per slab)
+    const uint32_t taddr_t = taddr + 2 * MW;
+#pragma unroll
+    for (int k = 0; k < MW; k += 4) {
+      const uint4 t4 = __ldg(reinterpret_cast<const uint4*>(P.ttab + (size_t)c * MW + k));
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr_t + k), "r"(t4.x),
+                   "r"(t4.y), "r"(t4.z), "r"(t4.w)
+                   : "memory");
+    }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     if (c == 0) {  // slot b starts at active tile b; fill the ring, prefetch tiles 3..5
       Cursor c0;
@@ -448,11 +487,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
           // the last consumer warp done with buffer b refills it (no consumer-wide barrier)
           __syncwarp();
           if ((c & 31) == 0) {
+#if V3_EMPTY_MBAR
+            // arrive on EMPTY[b]; the state returned is the barrier's state before this
+            // arrival, so a pending count of 1 identifies the last warp (exactly one)
+            uint64_t st;
+            uint32_t pend;
+            asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];"
+                         : "=l"(st)
+                         : "r"(smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b))
+                         : "memory");
+            asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pend) : "l"(st));
+            if (pend == 1) tma_issue(P, slots[b], b, smem);
+#else
             const int done = atomicAdd(&slots[b].count, 1);
             if (done == NCONS / 32 - 1) {
               slots[b].count = 0;
               tma_issue(P, slots[b], b, smem);
             }
+#endif
           }
           if (c == 0) { V3_TRACE(2, f, 3) }
           ++f;
@@ -465,23 +517,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
         }
       }
       // ---- slab epilogue: undo the frame sign of the last step, write ----
+      if (c == 0 && f > 0) { V3_TRACE(2, f - 1, 4) }
       const uint32_t jlast = (uint32_t)gray(np - 1);
       const bool second = col >= P.ncols0;
       float* __restrict__ outp = second ? P.src[1].out : P.src[0].out;
       const int64_t ldo = second ? P.src[1].ldo : P.src[0].ldo;
       const int64_t lc = second ? col - P.ncols0 : col;
-#pragma unroll
-      for (int q = 0; q < RPT; ++q) {
-        const int pk = P.perm[q * NCONS + c];
-        if (pk >= 0) {
-          const int t = pk & 0xffff;
-          const uint32_t kmid = (uint32_t)pk >> 16;
-          const float a = flipf(acc[q], (uint32_t)(__popc(kmid & jlast) & 1) << 31);
-          if (P.direct) outp[lc * ldo + t] = a * P.scale;
-          else P.partials[((int64_t)(s - P.s_lo32) * P.total_cols + col) * P.r + t] = a;
+      // frame sign of slot q: popc(k_mid & jlast) odd = XOR of the k_mid bit masks of jlast's bits
+      uint2 fm = make_uint2(0u, 0u);
+      for (int l = 0; l < P.log_j; ++l)
+        if ((jlast >> l) & 1u) {
+          const uint2 m = masks_s[l * NCONS + c];
+          fm.x ^= m.x;
+          fm.y ^= m.y;
         }
-        acc[q] = 0.f;
+      float* __restrict__ dst = P.direct ? outp + lc * ldo : P.partials + ((int64_t)(s - P.s_lo32) * P.total_cols + col) * P.r;
+      const float sc = P.direct ? P.scale : 1.f;
+#pragma unroll
+      for (int k = 0; k < MW; k += 4) {
+        uint32_t tw[4];
+        tmem_ld<4>(taddr_t + k, tw);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int q = 2 * k + i;
+          const uint32_t t = (tw[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+          const uint32_t mw = q < 32 ? fm.x : fm.y;
+          if (t != 0xffffu) dst[t] = flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u) * sc;
+          acc[q] = 0.f;
+        }
       }
+      if (c == 0 && f > 0) { V3_TRACE(2, f - 1, 5) }
     }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");  // the last look-ahead load
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
