@@ -134,9 +134,10 @@ srht_status srht_plan_copy_indices(const srht_plan* plan, int64_t problem,
 srht_status srht_plan_copy_signs(const srht_plan* plan, int64_t problem,
                                  uint64_t* host_words);
 
-/* Device scratch bytes needed by srht_sketch* for `ncols` columns (the
- * per-slab partial sums of the multi-pass path; 0 when not needed).  The
- * workspace must be 256-byte aligned.                                        */
+/* Device scratch bytes needed by srht_sketch* for `ncols` columns: the
+ * per-slab partial sums that the fixed-order slab reduction finishes (the
+ * dense TMA kernel always writes them, in its slot order, even for a single
+ * slab; 0 when no path needs them).  The workspace must be 256-byte aligned. */
 size_t srht_workspace_bytes(const srht_plan* plan, int64_t ncols);
 
 /* Sketch one problem: SA (r x A->cols, column-major, ldsa >= r) = H~ D A and

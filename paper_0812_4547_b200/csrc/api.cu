@@ -61,8 +61,11 @@ size_t partial_bytes(const srht_plan* P, int64_t ncols, bool shards = false) {
   }
   int64_t S = P->S_act;
   if (P->ws_ok && P->S_act2 > S) S = P->S_act2;
-  if (S < min_s) return 0;
-  const size_t b = (size_t)S * (size_t)ncols * (size_t)P->r * sizeof(float);
+  size_t b = S < min_s ? 0 : (size_t)S * (size_t)ncols * (size_t)P->r * sizeof(float);
+  if (P->ws_ok && P->v3_ok) {  // kernel v3: slot-order partials of every slab, even a single one
+    const size_t b3 = (size_t)P->S_act2 * (size_t)ncols * (size_t)P->rpt2 * 256 * sizeof(float);
+    if (b3 > b) b = b3;
+  }
   return (b + 255) & ~size_t(255);
 }
 
@@ -240,7 +243,6 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       vp.total_cols = rp.total_cols;
       vp.signs = P->d_signs3;
       vp.meta = P->d_meta3;
-      vp.ttab = P->d_ttab3;
       vp.masks = P->d_masks3;
       vp.log_j = P->log_j2;
       vp.r = P->r;
@@ -254,9 +256,7 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       vp.s_lo32 = (int)s_lo2;
       vp.J32 = (int)vp.J;
       vp.n_sub32 = (int)vp.n_sub;
-      vp.scale = P->scale;
       vp.partials = sp.partials;
-      vp.direct = direct;
       vp.trace = srht::g_debug_trace;
       vp.debug = srht::g_debug_mode;
       e = srht::launch_sketch_tma(P, vp, st);
@@ -288,7 +288,11 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
     }
     if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot + 1], st);
     if (e != cudaSuccess) return SRHT_ECUDA;
-    if (!direct && srht::launch_reduce(rp, 14 + P->log_j2, st) != cudaSuccess) return SRHT_ECUDA;
+    if (v3) {  // slot-order partials, always reduced (also for a single slab)
+      if (srht::launch_reduce_v3(rp, P->d_ttab3, P->rpt2, 14 + P->log_j2, st) != cudaSuccess) return SRHT_ECUDA;
+    } else if (!direct && srht::launch_reduce(rp, 14 + P->log_j2, st) != cudaSuccess) {
+      return SRHT_ECUDA;
+    }
     return SRHT_OK;
   }
   return srht::launch_sketch(P, sp, st) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;

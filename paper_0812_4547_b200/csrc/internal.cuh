@@ -120,20 +120,20 @@ struct V3Params {
   int64_t ncols0, total_cols;
   const uint4* signs;     // plan d_signs3
   const uint32_t* meta;   // plan d_meta3
-  const uint32_t* ttab;   // plan d_ttab3
   const uint2* masks;     // plan d_masks3
   int log_j;
   int64_t r, n;
   int64_t J, n_sub, S_act;  // S_act: slabs of this launch, global slabs s_lo ..
   int64_t n_items;        // total_cols * S_act
   int n_items32, S_act32, J32, n_sub32, s_lo32;  // the same, 32-bit (checked on the host)
-  float scale;
-  float* partials;        // [S_act][total_cols][r] when S_act > 1 or direct == 0
-  int direct;             // 1: single slab, write r^{-1/2} * sum straight to the output
+  float* partials;        // [S_act][total_cols][rpt2 * 256], slot order (k_reduce_v3 finishes)
   unsigned long long* trace;  // experiment phase timestamps (srht_debug_set_trace), else null
   int debug;                  // experiment knock-outs (srht_debug_set_mode, debug build), else 0
 };
 cudaError_t launch_sketch_tma(const srht_plan* P, const V3Params& vp, cudaStream_t stream);
+// Slab reduction of kernel v3's slot-order partials (sp.partials, S_act, s_lo, outputs).
+cudaError_t launch_reduce_v3(const SketchParams& sp, const uint32_t* ttab, int rpt, int slab_shift,
+                             cudaStream_t stream);
 int v3_mid(int x);  // kernel-v3 z layout (host side, for the slot layout)
 extern int g_kernel_force;  // 0 auto, 2 = kernel v2 instead of v3 (srht_debug_set_kernel)
 extern int g_last_kernel;   // 1/2/3: tile kernel of the last srht_sketch* call (bench labels)

@@ -268,9 +268,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + CTRL_TMEM);
   SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + CTRL_SLOTS);
   constexpr int MW = RPT / 2;                        // packed meta words (TMEM columns) per consumer thread
-  // TMEM columns: gather offsets [0, 2 MW) then output rows [2 MW, 4 MW) (two consumer
-  // warps per lane quarter, MW columns each)
-  constexpr int TCOLS = (4 * MW) < 32 ? 32 : 4 * MW;
+  constexpr int TCOLS = (2 * MW) < 32 ? 32 : 2 * MW; // TMEM columns allocated (two consumer warps per lane quarter)
   const int tid = threadIdx.x;
 
   // ---------------- setup (all threads) ----------------
@@ -420,17 +418,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
                    "r"(m4.y), "r"(m4.z), "r"(m4.w)
                    : "memory");
     }
-    // output rows (slab epilogue) -> TMEM (once): a global load per output there would
-    // serialise behind the output stores (measured ~29 us per slab)
-    const uint32_t taddr_t = taddr + 2 * MW;
-#pragma unroll
-    for (int k = 0; k < MW; k += 4) {
-      const uint4 t4 = __ldg(reinterpret_cast<const uint4*>(P.ttab + (size_t)c * MW + k));
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr_t + k), "r"(t4.x),
-                   "r"(t4.y), "r"(t4.z), "r"(t4.w)
-                   : "memory");
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     if (c == 0) {  // slot b starts at active tile b; fill the ring, prefetch tiles 3..5
       Cursor c0;
       cursor_start(P, c0);
@@ -516,13 +503,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
           }
         }
       }
-      // ---- slab epilogue: undo the frame sign of the last step, write ----
+      // ---- slab epilogue: undo the frame sign of the last step; write the partial in slot
+      // order (coalesced; k_reduce_v3 maps slots to output rows).  Writing rows t here
+      // directly would scatter 32 lines per store instruction (measured 8 us per slab).
       if (c == 0 && f > 0) { V3_TRACE(2, f - 1, 4) }
       const uint32_t jlast = (uint32_t)gray(np - 1);
-      const bool second = col >= P.ncols0;
-      float* __restrict__ outp = second ? P.src[1].out : P.src[0].out;
-      const int64_t ldo = second ? P.src[1].ldo : P.src[0].ldo;
-      const int64_t lc = second ? col - P.ncols0 : col;
       // frame sign of slot q: popc(k_mid & jlast) odd = XOR of the k_mid bit masks of jlast's bits
       uint2 fm = make_uint2(0u, 0u);
       for (int l = 0; l < P.log_j; ++l)
@@ -531,21 +516,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
           fm.x ^= m.x;
           fm.y ^= m.y;
         }
-      float* __restrict__ dst = P.direct ? outp + lc * ldo : P.partials + ((int64_t)(s - P.s_lo32) * P.total_cols + col) * P.r;
-      const float sc = P.direct ? P.scale : 1.f;
+      float* __restrict__ dst = P.partials + ((int64_t)(s - P.s_lo32) * P.total_cols + col) * (RPT * NCONS) + c;
 #pragma unroll
-      for (int k = 0; k < MW; k += 4) {
-        uint32_t tw[4];
-        tmem_ld<4>(taddr_t + k, tw);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int q = 2 * k + i;
-          const uint32_t t = (tw[i >> 1] >> (16 * (i & 1))) & 0xffffu;
-          const uint32_t mw = q < 32 ? fm.x : fm.y;
-          if (t != 0xffffu) dst[t] = flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u) * sc;
-          acc[q] = 0.f;
-        }
+      for (int q = 0; q < RPT; ++q) {
+        const uint32_t mw = q < 32 ? fm.x : fm.y;
+        dst[q * NCONS] = flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u);
+        acc[q] = 0.f;
       }
       if (c == 0 && f > 0) { V3_TRACE(2, f - 1, 5) }
     }
@@ -596,6 +572,45 @@ cudaError_t launch_rpt(const V3Params& vp, int grid, cudaStream_t stream) {
 }  // namespace v3
 
 int v3_mid(int x) { return v3::mid(x); }
+
+namespace {
+// Fixed-order slab reduction of kernel v3's slot-order partials: thread j = slot (q, c)
+// = q * 256 + c finds its output row t in the plan's t table, then sums the slab
+// partials exactly like k_reduce_slabs (FP64, slabs in order, slab sign of K[t]; DESIGN.md
+// reading R10), so results do not depend on the slot layout.
+__global__ void k_reduce_v3(const __grid_constant__ SketchParams P, const uint32_t* __restrict__ ttab, int rpt,
+                            int slab_shift) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t col = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  const int64_t slots = (int64_t)rpt * 256;
+  if (j >= slots || col >= P.total_cols) return;
+  const int q = (int)(j >> 8), c = (int)(j & 255);
+  const uint32_t t = (ttab[(size_t)c * (rpt / 2) + (q >> 1)] >> (16 * (q & 1))) & 0xffffu;
+  if (t == 0xffffu) return;  // empty slot
+  const uint32_t ks = (uint32_t)(P.K[t] >> slab_shift);
+  double sum = 0.0;
+  for (int64_t s = 0; s < P.S_act; ++s) {
+    const uint32_t v = __float_as_uint(P.partials[(s * P.total_cols + col) * slots + j]);
+    sum += (double)__uint_as_float(v ^ ((uint32_t)(__popc(ks & (uint32_t)(P.s_lo + s)) & 1) << 31));
+  }
+  if (P.part_out) {  // row shard: unscaled partial, summed across shards by the caller
+    P.part_out[col * P.ldp + t] = sum;
+    return;
+  }
+  const bool second = col >= P.ncols0;
+  const ColSrc& cs = second ? P.src[1] : P.src[0];
+  const int64_t lc = second ? col - P.ncols0 : col;
+  cs.out[lc * cs.ldo + t] = (float)(sum * P.scale_f64);
+}
+}  // namespace
+
+cudaError_t launch_reduce_v3(const SketchParams& sp, const uint32_t* ttab, int rpt, int slab_shift,
+                             cudaStream_t stream) {
+  const int64_t zc = (sp.total_cols + 65534) / 65535;
+  const dim3 grid((unsigned)rpt, (unsigned)(sp.total_cols < 65535 ? sp.total_cols : 65535), (unsigned)zc);
+  k_reduce_v3<<<grid, 256, 0, stream>>>(sp, ttab, rpt, slab_shift);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sketch_tma(const srht_plan* P, const V3Params& vp, cudaStream_t stream) {
   if (vp.total_cols <= 0) return cudaSuccess;
