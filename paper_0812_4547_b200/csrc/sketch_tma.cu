@@ -56,6 +56,13 @@ constexpr int CTRL_OFF = MASK_OFF + V3_MAX_LOGJ * NCONS * 8;
 // FULL mbarriers: NQ per buffer, one per contiguous 1/NQ of the tile (round 1 reads the
 // tile quarter by quarter, so it starts as soon as the first quarter has landed).
 constexpr int NQ = V3_QSPLIT ? 4 : 1;
+// Split issue: the refill copies quarter 0 (and the D bits) only; the producer thread that
+// sees quarter 0 land copies quarters 1..3 (a lone quarter lands ~4x sooner than four
+// concurrent ones, and the later quarters are needed ~700 cycles apart).
+#ifndef V3_SPLIT_ISSUE
+#define V3_SPLIT_ISSUE 1
+#endif
+constexpr bool SPLIT = V3_SPLIT_ISSUE && NQ == 4;
 // control block: FULL mbarriers [0, 8 NQ NBUF), TMEM address [96,100), EMPTY mbarriers
 // [104,128), slot states [128,..)
 constexpr int CTRL_TMEM = 96, CTRL_EMPTY = 104, CTRL_SLOTS = 128, CTRL_BYTES = 384;
@@ -189,6 +196,7 @@ __device__ __forceinline__ const float* col_ptr(const V3Params& P, int col) {
 struct SlotState {
   Cursor cur;   // next tile for this slot
   int count;    // consumer warps done with the slot's current tile (atomic refill)
+  int f;        // flat index of that tile (trace builds)
 };
 #ifndef V3_L2_HINTS
 #define V3_L2_HINTS 1
@@ -202,9 +210,12 @@ __device__ __forceinline__ void tile_src(const V3Params& P, const Cursor& c, int
   src = col_ptr(P, c.col) + row0;
 }
 
+template <int DBG>
 __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int b, unsigned char* smem) {
   Cursor c = st.cur;
   if (c.it >= P.n_items32) return;
+  if ((DBG & 1) && blockIdx.x == 0 && st.f < 4096) P.trace[((size_t)2 * 4096 + st.f) * 8 + 6] = clock64();
+  st.f += NBUF;
   const uint32_t bar = smem_u32(smem + CTRL_OFF + 8 * NQ * b);  // quarter q: bar + 8 q
   int tile;
   const float* src;
@@ -212,7 +223,7 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
   tile_src(P, c, tile, src, full);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {  // signs ride with the first part; a tail tile has no data parts
+  for (int q = 0; q < (SPLIT ? 1 : NQ); ++q) {  // signs ride with the first part; a tail tile has no data parts
     const int bytes = (full ? B * 4 / NQ : 0) + (q == 0 ? 2048 : 0);
     if (bytes)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar + 8 * q), "r"(bytes) : "memory");
@@ -235,7 +246,7 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
   if (full) {  // a tail tile is loaded by the producers themselves (guarded)
     const uint32_t dst = smem_u32(smem + (size_t)b * BUF_BYTES);
 #pragma unroll
-    for (int k = 0; k < 4; ++k)  // 16 KB each (the bulk-copy size limit is 1 MB; 16 KB keeps parts even)
+    for (int k = 0; k < (SPLIT ? 1 : 4); ++k)  // 16 KB each
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], 16384, [%2], %3;" ::"r"(
               dst + k * 16384),
@@ -314,6 +325,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       const uint32_t fullb = smem_u32(smem + CTRL_OFF + 8 * NQ * b);
       mbar_wait(fullb, parity);  // first part (and the signs)
       if (p == 0) { V3_TRACE(g, f, 6) }
+      if (SPLIT && p == 0) {  // quarters 1..3 (data-less for a tail tile)
+        const bool full_tile = row0 + B <= n;
+        uint64_t stream;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream));
+        const uint32_t dst = smem_u32(buf);
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+          if (full_tile) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16384;" ::"r"(fullb + 8 * q) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], 16384, [%2], %3;" ::"r"(
+                    dst + q * 16384),
+                "l"(colp + row0 + q * 4096), "r"(fullb + 8 * q), "l"(stream)
+                : "memory");
+          } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fullb + 8 * q) : "memory");
+          }
+        }
+      }
       if (DBG & 16) {  // knock-out: data movement only (no transform at all)
         for (int q = 1; q < NQ; ++q) mbar_wait(fullb + 8 * q, parity);
         bar_arrive(BAR_READY0 + b, 384);
@@ -424,9 +454,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       for (int b = 0; b < NBUF; ++b) {
         slots[b].cur = c0;
         slots[b].count = 0;
+        slots[b].f = b;
         cursor_next_active(P, c0);
       }
-      for (int b = 0; b < NBUF; ++b) tma_issue(P, slots[b], b, smem);
+      for (int b = 0; b < NBUF; ++b) tma_issue<DBG>(P, slots[b], b, smem);
     }
     float acc[RPT];
 #pragma unroll
@@ -484,12 +515,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
                          : "r"(smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b))
                          : "memory");
             asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pend) : "l"(st));
-            if (pend == 1) tma_issue(P, slots[b], b, smem);
+            if (pend == 1) tma_issue<DBG>(P, slots[b], b, smem);
 #else
             const int done = atomicAdd(&slots[b].count, 1);
             if (done == NCONS / 32 - 1) {
               slots[b].count = 0;
-              tma_issue(P, slots[b], b, smem);
+              tma_issue<DBG>(P, slots[b], b, smem);
             }
 #endif
           }

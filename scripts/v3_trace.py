@@ -71,3 +71,18 @@ ep = tt[2][(tt[2][:, 4] > 0)]
 if len(ep):
     e = ep[:, 5] - ep[:, 4]
     print("consumer slab epilogue (%d items): mean %.0f median %.0f max %.0f" % (len(e), e.mean(), np.median(e), e.max()))
+# TMA latency: refill issue (consumer trace slot 6, indexed by the loaded tile) to the
+# producer's FULL wait completing (producer slot 6); when the producer did not wait only
+# the lead (issue -> producer starts waiting) is known
+iss = tt[2, :, 6]
+lat, lead = [], []
+for f in range(3, T):
+    g = f % 2
+    if iss[f] > 0 and tt[g, f, 6] > 0 and tt[g, f, 0] > 0:
+        lead.append(tt[g, f, 0] - iss[f])
+        if tt[g, f, 6] - tt[g, f, 0] > 300:
+            lat.append(tt[g, f, 6] - iss[f])
+if lead:
+    print("refill lead (issue -> producer starts waiting): median %.0f p10 %.0f p90 %.0f" % (np.median(lead), np.percentile(lead, 10), np.percentile(lead, 90)))
+if lat:
+    print("refill latency when the producer waited (%d of %d tiles): median %.0f p10 %.0f p90 %.0f" % (len(lat), len(lead), np.median(lat), np.percentile(lat, 10), np.percentile(lat, 90)))
