@@ -124,14 +124,14 @@ cudaError_t build_ws_layout(srht_plan* P, const std::vector<int32_t>& K) {
   return e;
 }
 
-// Kernel v3: per consumer thread c, rpt2/2 words of two 15-bit mid-layout word
-// offsets (slot q = 2i in bits 0..14, 2i+1 in bits 17..31 of word i); ttab, the
-// same shape: the two slots' output rows t (bits 0..15, 16..31; 0xffff = empty slot);
-// masks[sh][c] bit q = bit sh of k_mid of slot (q, c).
+// Kernel v3: per consumer thread c, rpt2 words: the byte offset of slot q's z value in
+// the tile buffer (mid layout); ttab: per thread rpt2/2 words holding the output rows t
+// of slots 2i, 2i+1 (bits 0..15, 16..31; 0xffff = empty slot); masks[sh][c] bit q = bit
+// sh of k_mid of slot (q, c).
 cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
   const int rpt = P->rpt2, slots = rpt * 256, mw = rpt / 2;
   const std::vector<int32_t> slot_t = deal_slots(K, rpt, srht::v3_mid);
-  std::vector<uint32_t> meta((size_t)256 * mw, 0u);
+  std::vector<uint32_t> meta((size_t)256 * rpt, 0u);
   std::vector<uint32_t> ttab((size_t)256 * mw, 0xffffffffu);
   std::vector<uint2> masks((size_t)(P->log_j2 > 0 ? P->log_j2 : 1) * 256, make_uint2(0u, 0u));
   for (int q = 0; q < rpt; ++q)
@@ -141,7 +141,7 @@ cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
       const int k = K[t];
       const uint32_t off = (uint32_t)srht::v3_mid(k & ((1 << 14) - 1));
       const uint32_t kmid = (uint32_t)(k >> 14) & (uint32_t)(P->J2 - 1);
-      meta[(size_t)c * mw + q / 2] |= off << (17 * (q & 1));  // lo | hi << 17
+      meta[(size_t)c * rpt + q] = off * 4u;  // byte offset in the tile buffer
       uint32_t& tw = ttab[(size_t)c * mw + q / 2];
       tw = (tw & ~(0xffffu << (16 * (q & 1)))) | ((uint32_t)t << (16 * (q & 1)));
       for (int sh = 0; sh < P->log_j2; ++sh)

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
   uint2* masks_s = reinterpret_cast<uint2*>(smem + MASK_OFF);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + CTRL_TMEM);
   SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + CTRL_SLOTS);
-  constexpr int MW = RPT / 2;                        // packed meta words (TMEM columns) per consumer thread
+  constexpr int MW = RPT;                            // gather byte offsets (TMEM columns) per consumer thread
   constexpr int TCOLS = (2 * MW) < 32 ? 32 : 2 * MW; // TMEM columns allocated (two consumer warps per lane quarter)
   const int tid = threadIdx.x;
 
@@ -490,15 +490,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
             if (k == 0 && c == 0) { V3_TRACE(2, f, 1) }
             const uint32_t* wk = w[(k / CH) & 1];
 #pragma unroll
-            for (int i = 0; i < 2 * CH; ++i) {
-              const int q = 2 * k + i;
-              // word = lo | hi << 17 (15-bit word offsets; bits 15, 16 clear), so the high
-              // sample's byte offset is w >> 15
-              const float z = (DBG & 2) ? __uint_as_float(wk[i >> 1] & 0x3fffffffu)
-                              : (i & 1) ? *reinterpret_cast<const float*>(reinterpret_cast<const char*>(buf) + (wk[i >> 1] >> 15))
-                                        : buf[wk[i >> 1] & 0x7fffu];
+            for (int i = 0; i < CH; i += 2) {
+              const int q = k + i;
+              // one byte offset per slot (no address arithmetic); a pair of slots is
+              // accumulated by one FADD2
+              const char* bb = reinterpret_cast<const char*>(buf);
+              const float z0 = (DBG & 2) ? __uint_as_float(wk[i] & 0x3fffffffu) : *reinterpret_cast<const float*>(bb + wk[i]);
+              const float z1 =
+                  (DBG & 2) ? __uint_as_float(wk[i + 1] & 0x3fffffffu) : *reinterpret_cast<const float*>(bb + wk[i + 1]);
               const uint32_t mw = q < 32 ? mk.x : mk.y;
-              acc[q] = flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u) + z;
+              const float2 a = make_float2(flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u),
+                                           flipf(acc[q + 1], __funnelshift_l(mw, mw, 30 - (q & 31)) & 0x80000000u));
+              const float2 sum = __fadd2_rn(a, make_float2(z0, z1));
+              acc[q] = sum.x;
+              acc[q + 1] = sum.y;
             }
           }
           if (c == 0) { V3_TRACE(2, f, 2) }
