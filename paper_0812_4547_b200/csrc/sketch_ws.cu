@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
       const int64_t lc = second ? col - P.ncols0 : col;
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
-        const int t = P.perm[q * NCONS + c];
+        const int t = __ldg(P.perm + q * NCONS + c);  // read-only: may be batched ahead of the stores
         if (t >= 0) {
           const uint32_t kmid = __brev(mrow[q * NCONS]) & (uint32_t)(P.J - 1);
           const float a = flipf(acc[q], (uint32_t)(__popc(kmid & jlast) & 1) << 31);
