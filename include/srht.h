@@ -208,8 +208,11 @@ srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM,
  * Cholesky factorization of Q_PP (needs a full-column-rank SA, the generic case
  * for r >= d+1).  x_p (d FP64) at x + p*stride_x; iters[p] (device, may be NULL)
  * = outer iterations, or -1 (iteration cap), -2 (inner loop cap), -3 (Q_PP not
- * positive definite).  One CTA per problem.  Workspace: the Cholesky factors
- * when d > 160 (srht_nnls_workspace_bytes; 0 otherwise), 8-byte aligned.
+ * positive definite).  One CTA per problem; the factor is updated
+ * incrementally (append / delete with Givens rotations), in shared memory for
+ * d <= 160, else in the workspace (two d x d FP64 slots per problem, row-major,
+ * blocked 32-row triangular solves; srht_nnls_workspace_bytes; 0 for d <= 160),
+ * 8-byte aligned.
  * Device pointers; asynchronous on `stream`.                                  */
 size_t srht_nnls_workspace_bytes(int64_t d, int64_t batch);
 srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G,

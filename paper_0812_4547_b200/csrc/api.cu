@@ -597,7 +597,7 @@ srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int6
 
 size_t srht_nnls_workspace_bytes(int64_t d, int64_t batch) {
   if (d < 1 || batch < 1 || srht::nnls_factor_in_smem(d)) return 0;
-  return (size_t)batch * (size_t)d * (size_t)d * sizeof(double);
+  return (size_t)batch * 2 * (size_t)d * (size_t)d * sizeof(double);  // two factor slots per problem
 }
 
 srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,

@@ -17,8 +17,9 @@
 //
 // One CTA (256 threads) per problem, FP64 throughout: all threads for the dual w = q - Q x
 // and the argmax/argmin reductions, warp 0 for the factor updates and the triangular solves.
-// This incremental form runs when L fits in shared memory (d <= 160); larger d uses
-// k_nnls_lh_refactor below with the factor in the caller's workspace.  Q is read from G (L2).
+// This form runs when L fits in shared memory (d <= 160); larger d uses k_nnls_lh_big below
+// (the same updates, factor row-major in the caller's workspace, blocked CTA-wide solves).
+// Q is read from G (L2).
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -318,34 +319,115 @@ __global__ void __launch_bounds__(NT) k_nnls_lh(int d, const double* __restrict_
   if (tid == 0 && iters) iters[p] = status ? status : it;
 }
 
-// Large d (factor in the workspace, L2): the passive-set system is refactored from scratch in
-// every inner step (O(m^3) spread over the CTA); the incremental updates of k_nnls_lh would
-// serialise O(m^2) dependent L2 round trips per step there.
-__global__ void __launch_bounds__(NT) k_nnls_lh_refactor(int d, const double* __restrict__ Gall, int64_t ldg, int64_t stride_g,
-                                               double* __restrict__ xall, int64_t stride_x, int32_t* __restrict__ iters,
-                                               double* __restrict__ ws, int64_t batch) {
+// ---------------------------------------------------------------------------------------
+// Large d (factor does not fit in shared memory): the incremental Lawson-Hanson of
+// k_nnls_lh with the factor in the workspace ROW-major (L[a][b] at F[a*d + b], b <= a) and
+// CTA-wide blocked triangular solves, so every L2 access is a coalesced row segment or a
+// 32 x 32 diagonal block held in one warp's registers: O(m^2 / 32) sequential steps per
+// solve instead of O(m^2) dependent round trips.  A deletion copies the factor into the
+// second workspace half without row/column k, then restores it with Givens rotations.
+constexpr int BK = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// y[0..m) = L^{-1} b[0..m)   (b, y, part in shared memory; y may not alias b)
+__device__ void big_fwd(const double* __restrict__ F, int d, int m, const double* b, double* y, double* part) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int a0 = 0; a0 < m; a0 += BK) {
+    const int nb = m - a0 < BK ? m - a0 : BK;
+    for (int i = wid; i < nb; i += NT / 32) {  // part[i] = sum_{c < a0} L[a0+i][c] y[c]
+      const double* row = F + (size_t)(a0 + i) * d;
+      double acc = 0.0;
+      for (int c = lane; c < a0; c += 32) acc += row[c] * y[c];
+      acc = warp_sum(acc);
+      if (lane == 0) part[i] = acc;
+    }
+    __syncthreads();
+    if (wid == 0) {  // diagonal block: lane j holds row a0+j; column sweep
+      const bool act = lane < nb;
+      double Lr[BK];
+#pragma unroll
+      for (int i = 0; i < BK; ++i) Lr[i] = (act && i <= lane) ? F[(size_t)(a0 + lane) * d + a0 + i] : 1.0;
+      double rj = act ? b[a0 + lane] - part[lane] : 0.0, yj = 0.0;
+#pragma unroll
+      for (int i = 0; i < BK; ++i) {
+        if (i < nb) {
+          const double yi = __shfl_sync(0xffffffffu, rj / Lr[i], i);
+          if (lane == i) yj = yi;
+          if (lane > i) rj -= Lr[i] * yi;
+        }
+      }
+      if (act) y[a0 + lane] = yj;
+    }
+    __syncthreads();
+  }
+}
+
+// z[0..m) = L^{-T} y[0..m)   (y is consumed)
+__device__ void big_bwd(const double* __restrict__ F, int d, int m, double* y, double* z) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int a1 = m; a1 > 0;) {
+    const int a0 = ((a1 - 1) / BK) * BK, nb = a1 - a0;
+    if (wid == 0) {  // diagonal block: lane j holds column a0+j; column sweep from the bottom
+      const bool act = lane < nb;
+      double Lc[BK];
+#pragma unroll
+      for (int i = 0; i < BK; ++i) Lc[i] = (act && i < nb && i >= lane) ? F[(size_t)(a0 + i) * d + a0 + lane] : 1.0;
+      double rj = act ? y[a0 + lane] : 0.0, zj = 0.0;
+#pragma unroll
+      for (int i = BK - 1; i >= 0; --i) {
+        if (i < nb) {
+          const double zi = __shfl_sync(0xffffffffu, rj / Lc[i], i);
+          if (lane == i) zj = zi;
+          if (lane < i) rj -= Lc[i] * zi;
+        }
+      }
+      if (act) z[a0 + lane] = zj;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < a0; c += NT) {  // y[c] -= sum_{b in block} L[b][c] z[b]
+      double acc = 0.0;
+      for (int b = a0; b < a1; ++b) acc += F[(size_t)b * d + c] * z[b];
+      y[c] -= acc;
+    }
+    __syncthreads();
+    a1 = a0;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restrict__ Gall, int64_t ldg, int64_t stride_g,
+                                                   double* __restrict__ xall, int64_t stride_x, int32_t* __restrict__ iters,
+                                                   double* __restrict__ ws, int64_t batch) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ NnlsSmem s;
+  __shared__ double part[BK];
   const int64_t p = blockIdx.x + (int64_t)blockIdx.y * 65535;
   if (p >= batch) return;
   const double* __restrict__ G = Gall + p * stride_g;  // Q[i][j] = G[i + j*ldg], q[i] = G[i + d*ldg]
-  // shared: x, z, w (d each), P index list (d ints), flags; factor F (m x m, ld = d) in smem or ws
   double* x = dsm;
   double* z = x + d;
   double* w = z + d;
-  int* idx = reinterpret_cast<int*>(w + d);
-  unsigned char* passive = reinterpret_cast<unsigned char*>(idx + d);
+  double* zt = w + d;
+  double* bv = zt + d;
+  int* order = reinterpret_cast<int*>(bv + d);
+  unsigned char* passive = reinterpret_cast<unsigned char*>(order + d);
   unsigned char* skipped = passive + d;
-  double* F = ws + p * (int64_t)d * d;  // large d: the factor lives in the workspace
+  double* F = ws + p * 2 * (int64_t)d * d;  // two factor slots (deletions copy between them)
+  double* F2 = F + (int64_t)d * d;
   const int tid = threadIdx.x;
 
   for (int i = tid; i < d; i += NT) {
     x[i] = 0.0;
+    z[i] = 0.0;
     passive[i] = 0;
     skipped[i] = 0;
   }
-  // tol = 1e-10 max|q|
-  double qm = 0.0;
+  if (tid == 0) s.m = 0;
+  double qm = 0.0;  // tol = 1e-10 max|q|
   for (int i = tid; i < d; i += NT) qm = fmax(qm, fabs(G[i + d * ldg]));
   block_argmax(qm, 0, true, s);
   const double tol = 1e-10 * fmax(s.red_v[0], 2.2250738585072014e-308);
@@ -353,29 +435,56 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_refactor(int d, const double* __
   int it = 0;
   int status = 0;
   while (true) {
-    // w = q - Q x
-    for (int i = tid; i < d; i += NT) {
+    for (int i = tid; i < d; i += NT) {  // w = q - Q x (column i of G = row i of Q)
       double acc = G[i + d * ldg];
-      for (int j = 0; j < d; ++j) acc -= G[i + j * ldg] * x[j];  // column i of G = row i of Q
+      for (int j = 0; j < d; ++j) acc -= G[i + j * ldg] * x[j];
       w[i] = acc;
     }
     __syncthreads();
-    double bv = -INFINITY;
+    double bvv = -INFINITY;
     int bi = 0x7fffffff;
     for (int i = tid; i < d; i += NT)
-      if (!passive[i] && !skipped[i] && (w[i] > bv || (w[i] == bv && i < bi))) {
-        bv = w[i];
+      if (!passive[i] && !skipped[i] && (w[i] > bvv || (w[i] == bvv && i < bi))) {
+        bvv = w[i];
         bi = i;
       }
-    block_argmax(bv, bi, bi != 0x7fffffff, s);
+    block_argmax(bvv, bi, bi != 0x7fffffff, s);
     if (s.red_i[0] == 0x7fffffff || s.red_v[0] <= tol) break;
     if (++it > max_iter) {
       status = -1;
       break;
     }
     const int t = s.red_i[0];
-    if (tid == 0) passive[t] = 1;
-    __syncthreads();
+    {  // append t: row m of L = L^{-1} Q[order, t], diagonal sqrt(Q_tt - |row|^2)
+      const int m = s.m;
+      for (int a = tid; a < m; a += NT) bv[a] = G[order[a] + (int64_t)t * ldg];
+      __syncthreads();
+      big_fwd(F, d, m, bv, zt, part);
+      double ss = 0.0;
+      for (int a = tid; a < m; a += NT) ss += zt[a] * zt[a];
+      ss = warp_sum(ss);
+      __syncthreads();
+      if ((tid & 31) == 0) s.red_v[tid >> 5] = ss;
+      __syncthreads();
+      if (tid == 0) {
+        double tot = 0.0;
+        for (int k = 0; k < NT / 32; ++k) tot += s.red_v[k];
+        const double dd = G[t + (int64_t)t * ldg] - tot;
+        s.flag = dd > 0.0 ? 0 : 1;
+        if (dd > 0.0) {
+          F[(size_t)m * d + m] = sqrt(dd);
+          order[m] = t;
+          passive[t] = 1;
+          s.m = m + 1;
+        }
+      }
+      for (int a = tid; a < m; a += NT) F[(size_t)m * d + a] = zt[a];
+      __syncthreads();
+    }
+    if (s.flag) {  // Q_PP not positive definite: rank-deficient passive set
+      status = -3;
+      break;
+    }
     int inner = 0;
     while (true) {
       ++inner;
@@ -383,90 +492,37 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_refactor(int d, const double* __
         status = -2;
         break;
       }
-      // passive index list, ascending
-      if (tid == 0) {
-        int m = 0;
-        for (int j = 0; j < d; ++j)
-          if (passive[j]) idx[m++] = j;
-        s.m = m;
-      }
-      __syncthreads();
       const int m = s.m;
-      // F = Q_PP (lower triangle), then Cholesky in place: F F^T = Q_PP
-      for (int e = tid; e < m * m; e += NT) {
-        const int a = e / m, b = e % m;
-        if (b <= a) F[a + b * d] = G[idx[a] + idx[b] * ldg];
-      }
+      for (int a = tid; a < m; a += NT) bv[a] = G[order[a] + (int64_t)d * ldg];
       __syncthreads();
-      for (int k = 0; k < m; ++k) {
-        if (tid == 0) {
-          const double dk = F[k + k * d];
-          s.flag = dk > 0.0 ? 0 : 1;
-          F[k + k * d] = sqrt(dk > 0.0 ? dk : 1.0);
-        }
-        __syncthreads();
-        if (s.flag) break;
-        const double piv = F[k + k * d];
-        for (int a = k + 1 + tid; a < m; a += NT) F[a + k * d] /= piv;
-        __syncthreads();
-        const int rest = m - k - 1;
-        for (int e = tid; e < rest * rest; e += NT) {
-          const int a = k + 1 + e / rest, b = k + 1 + e % rest;
-          if (b <= a) F[a + b * d] -= F[a + k * d] * F[b + k * d];
-        }
-        __syncthreads();
-      }
-      if (s.flag) {  // Q_PP not positive definite: rank-deficient passive set
-        status = -3;
-        break;
-      }
-      // z_P: forward (F y = q_P) and back (F^T z = y) substitution, warp 0
-      if (tid < 32) {
-        for (int a = 0; a < m; ++a) {
-          double acc = 0.0;
-          for (int b = tid; b < a; b += 32) acc += F[a + b * d] * z[idx[b]];
-#pragma unroll
-          for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-          if (tid == 0) z[idx[a]] = (G[idx[a] + d * ldg] - acc) / F[a + a * d];
-          __syncwarp();
-        }
-        for (int a = m - 1; a >= 0; --a) {
-          double acc = 0.0;
-          for (int b = a + 1 + tid; b < m; b += 32) acc += F[b + a * d] * z[idx[b]];
-#pragma unroll
-          for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-          if (tid == 0) z[idx[a]] = (z[idx[a]] - acc) / F[a + a * d];
-          __syncwarp();
-        }
-      }
+      big_fwd(F, d, m, bv, zt, part);
+      big_bwd(F, d, m, zt, bv);  // z_P (in order positions) -> bv
+      for (int a = tid; a < m; a += NT) z[order[a]] = bv[a];
       __syncthreads();
-      for (int j = tid; j < d; j += NT)
-        if (!passive[j]) z[j] = 0.0;
-      // all z_P > 0?
       int bad = 0;
-      for (int a = tid; a < m; a += NT) bad |= z[idx[a]] <= 0.0;
+      for (int a = tid; a < m; a += NT) bad |= z[order[a]] <= 0.0;
       bad = __syncthreads_or(bad);
       if (!bad) {
         for (int j = tid; j < d; j += NT) {
-          x[j] = z[j];
+          x[j] = passive[j] ? z[j] : 0.0;
           skipped[j] = 0;
         }
         __syncthreads();
         break;
       }
-      if (inner == 1 && z[t] <= 0.0) {  // degenerate entry: leave x, do not offer t until x changes
+      if (inner == 1 && z[t] <= 0.0) {  // degenerate entry: t is the last appended; pop it
         if (tid == 0) {
           passive[t] = 0;
           skipped[t] = 1;
+          s.m -= 1;
         }
         __syncthreads();
         break;
       }
-      // step back: alpha = min over passive j with z_j <= 0 of x_j / (x_j - z_j)
-      double rv = INFINITY;
+      double rv = INFINITY;  // step back: alpha = min over passive j with z_j <= 0 of x_j / (x_j - z_j)
       int ri = 0x7fffffff;
       for (int a = tid; a < m; a += NT) {
-        const int j = idx[a];
+        const int j = order[a];
         if (z[j] <= 0.0) {
           const double ratio = x[j] / (x[j] - z[j]);
           if (ratio < rv || (ratio == rv && j < ri)) {
@@ -479,17 +535,57 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_refactor(int d, const double* __
       const double alpha = s.red_v[0];
       const int jstar = s.red_i[0];
       for (int j = tid; j < d; j += NT) {
+        if (!passive[j]) continue;
         double xj = x[j] + alpha * (z[j] - x[j]);
-        if (passive[j] && (xj <= 0.0 || j == jstar)) {
-          xj = 0.0;
-          passive[j] = 0;
-        }
+        if (xj <= 0.0 || j == jstar) xj = 0.0;
         x[j] = xj;
       }
-      int any = 0;
-      for (int j = tid; j < d; j += NT) any |= passive[j];
-      any = __syncthreads_or(any);
-      if (!any) break;
+      __syncthreads();
+      // delete the dropped positions, highest first
+      for (int k = s.m - 1; k >= 0; --k) {
+        if (x[order[k]] != 0.0) continue;  // uniform (shared x, synchronised)
+        const int mm = s.m, pp = mm - 1 - k;
+        for (int i = tid; i < pp; i += NT) zt[i] = F[(size_t)(k + 1 + i) * d + k];  // old column k below k
+        for (int e = tid; e < (mm - 1) * mm / 2 + mm; e += NT) {  // copy without row/column k
+          // e enumerates (i, j), j <= i < mm-1, row by row: i = floor((sqrt(8e+1)-1)/2)
+          int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+          while ((i + 1) * (i + 2) / 2 <= e) ++i;
+          while (i * (i + 1) / 2 > e) --i;
+          const int j = e - i * (i + 1) / 2;
+          if (i >= mm - 1) continue;
+          const int si = i < k ? i : i + 1, sj = j < k ? j : j + 1;
+          F2[(size_t)i * d + j] = F[(size_t)si * d + sj];
+        }
+        __syncthreads();
+        if (tid == 0) {
+          passive[order[k]] = 0;
+          for (int a = k; a < mm - 1; ++a) order[a] = order[a + 1];
+          s.m = mm - 1;
+        }
+        double* tmp = F;  // the copy is the factor now
+        F = F2;
+        F2 = tmp;
+        for (int j = 0; j < pp; ++j) {  // rank-1 update L22 L22^T + x x^T of rows/columns k..mm-2
+          const int jj = k + j;
+          __syncthreads();  // step j-1's updates (zt, column jj-1) are visible
+          if (tid == 0) {
+            const double ljj = F[(size_t)jj * d + jj], xj = zt[j];
+            const double rr = sqrt(ljj * ljj + xj * xj);
+            s.alpha = rr / ljj;  // c
+            part[0] = xj / ljj;  // s
+            F[(size_t)jj * d + jj] = rr;
+          }
+          __syncthreads();
+          const double c = s.alpha, sn = part[0];
+          for (int i = j + 1 + tid; i < pp; i += NT) {
+            const double lij = (F[(size_t)(k + i) * d + jj] + sn * zt[i]) / c;
+            zt[i] = c * zt[i] - sn * lij;
+            F[(size_t)(k + i) * d + jj] = lij;
+          }
+        }
+        __syncthreads();
+      }
+      if (s.m == 0) break;
     }
     if (status) break;
   }
@@ -497,7 +593,6 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_refactor(int d, const double* __
   for (int j = tid; j < d; j += NT) xo[j] = x[j] < 1e-14 ? 0.0 : x[j];
   if (tid == 0 && iters) iters[p] = status ? status : it;
 }
-
 }  // namespace
 
 size_t nnls_smem_bytes(int64_t d, bool fac_in_smem) {
@@ -514,10 +609,10 @@ cudaError_t launch_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t 
   const bool fs = nnls_factor_in_smem(d);
   const dim3 grid((unsigned)(batch < 65535 ? batch : 65535), (unsigned)((batch + 65534) / 65535));
   if (!fs) {
-    const size_t smem = (size_t)(3 * d + (d * 6 + 15) / 8 + 1) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(k_nnls_lh_refactor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = (size_t)(5 * d + (d * 6 + 15) / 8 + 1) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_nnls_lh_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_nnls_lh_refactor<<<grid, NT, smem, stream>>>((int)d, G, ldg, stride_g, x, stride_x, iters, ws, batch);
+    k_nnls_lh_big<<<grid, NT, smem, stream>>>((int)d, G, ldg, stride_g, x, stride_x, iters, ws, batch);
     return cudaGetLastError();
   }
   const size_t smem = nnls_smem_bytes(d, true);

@@ -414,7 +414,7 @@ def _nnls_problem(rng, r, d, zeros):
     return SA, Sb
 
 
-@pytest.mark.parametrize("r,d,zeros", [(64, 8, 4), (512, 50, 20), (2048, 100, 50), (4096, 200, 100)])
+@pytest.mark.parametrize("r,d,zeros", [(64, 8, 4), (512, 50, 20), (2048, 100, 50), (4096, 200, 100), (2048, 300, 150)])
 def test_nnls_gram_matches_lawson_hanson(lib, r, d, zeros):
     from oracle import nnls
     rng = np.random.default_rng(d)
@@ -434,6 +434,19 @@ def test_nnls_gram_matches_lawson_hanson(lib, r, d, zeros):
     if d <= 10:
         xb = nnls.nnls_bruteforce(A64, b64)
         assert abs(f(x) - f(xb)) <= 1e-10 * f(xb)
+
+
+def test_nnls_gram_large_d_deterministic(lib):
+    # d > 160 (factor in the workspace, CTA-wide blocked solves, deletions with Givens):
+    # repeated runs must agree bit for bit (a race in the shared updates would not)
+    rng = np.random.default_rng(7)
+    SA, Sb = _nnls_problem(rng, 1024, 240, 120)
+    G = lib.gram(to_dev(np.column_stack([SA, Sb])))
+    x0, it0 = lib.nnls_gram(G)
+    for _ in range(3):
+        x1, it1 = lib.nnls_gram(G)
+        assert int(it1) == int(it0)
+        assert torch.equal(x1, x0)
 
 
 def test_randomized_nnls_end_to_end_on_gpu(lib):
