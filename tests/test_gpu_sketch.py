@@ -439,6 +439,7 @@ def test_nnls_gram_matches_lawson_hanson(lib, r, d, zeros):
 def test_nnls_gram_large_d_deterministic(lib):
     # d > 160 (factor in the workspace, CTA-wide blocked solves, deletions with Givens):
     # repeated runs must agree bit for bit (a race in the shared updates would not)
+    import torch
     rng = np.random.default_rng(7)
     SA, Sb = _nnls_problem(rng, 1024, 240, 120)
     G = lib.gram(to_dev(np.column_stack([SA, Sb])))
