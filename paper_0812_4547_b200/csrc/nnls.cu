@@ -15,10 +15,10 @@
 // block restored by a rank-1 Cholesky update (O(m^2)); the passive set is stored in
 // insertion order, which changes only the rounding, not the solution.
 //
-// One CTA (256 threads) per problem, FP64 throughout: all threads for the dual w = q - Q x
-// and the argmax/argmin reductions, warp 0 for the factor updates and the triangular solves.
-// This form runs when L fits in shared memory (d <= 160); larger d uses k_nnls_lh_big below
-// (the same updates, factor row-major in the caller's workspace, blocked CTA-wide solves).
+// One CTA (256 threads) per problem, FP64 throughout (k_nnls_lh_big): all threads for the
+// dual w = q - Q x and the argmax/argmin reductions; the factor is row-major, in shared
+// memory while it fits (d <= ~155) else in the caller's workspace, and the triangular
+// solves are blocked (32-row diagonal blocks in one warp's registers, the rest CTA-wide).
 // Q is read from G (L2).
 #include <cuda_runtime.h>
 #include <math.h>
@@ -29,8 +29,6 @@ namespace srht {
 namespace {
 
 constexpr int NT = 256;
-// x, z, w, zt (d doubles each) + order (d ints) + passive, skipped (d bytes each), in doubles
-#define NNLS_VEC_DOUBLES(d) (4 * (int64_t)(d) + ((int64_t)(d) * 6 + 7) / 8 + 1)
 
 struct NnlsSmem {
   double red_v[NT / 32];
@@ -78,255 +76,16 @@ __device__ void block_argmin(double v, int i, bool ok, NnlsSmem& s) {
   __syncthreads();
 }
 
-// ---- warp-0 helpers on the factor L (column-major, ld = d: L[i][j] at F[i + j*d]) ----
-
-// Append index t: row m of L = L^{-1} Q[order, t], diagonal sqrt(Q_tt - |row|^2).
-// Returns false (L unchanged) when the new pivot is not positive.
-__device__ bool chol_append(double* F, int d, int* order, int m, int t, const double* G, int64_t ldg) {
-  const int lane = threadIdx.x & 31;
-  for (int a = 0; a < m; ++a) {
-    double acc = 0.0;
-    for (int b = lane; b < a; b += 32) acc += F[a + b * d] * F[m + b * d];
-#pragma unroll
-    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) F[m + a * d] = (G[order[a] + (int64_t)t * ldg] - acc) / F[a + a * d];
-    __syncwarp();
-  }
-  double ss = 0.0;
-  for (int b = lane; b < m; b += 32) ss += F[m + b * d] * F[m + b * d];
-#pragma unroll
-  for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-  const double dd = G[t + (int64_t)t * ldg] - ss;
-  if (!(dd > 0.0)) return false;
-  if (lane == 0) {
-    F[m + m * d] = sqrt(dd);
-    order[m] = t;
-  }
-  __syncwarp();
-  return true;
-}
-
-// Delete position k of the passive list (m entries): shift rows/columns, then restore the
-// trailing block with the rank-1 update L' L'^T = L22 L22^T + x x^T, x = old L[k+1.., k].
-__device__ void chol_delete(double* F, int d, int* order, int m, int k, double* xt) {
-  const int lane = threadIdx.x & 31;
-  const int p = m - 1 - k;
-  for (int i = lane; i < p; i += 32) xt[i] = F[k + 1 + i + k * d];
-  __syncwarp();
-  for (int j = 0; j < k; ++j)  // columns left of k: rows k+1.. move up by one
-    for (int i0 = k; i0 < m - 1; i0 += 32) {
-      const int i = i0 + lane;
-      const double v = i < m - 1 ? F[i + 1 + j * d] : 0.0;
-      __syncwarp();
-      if (i < m - 1) F[i + j * d] = v;
-      __syncwarp();
-    }
-  for (int j = k; j < m - 1; ++j)  // trailing block: (i+1, j+1) -> (i, j), lower triangle
-    for (int i0 = j; i0 < m - 1; i0 += 32) {
-      const int i = i0 + lane;
-      const double v = i < m - 1 ? F[i + 1 + (j + 1) * d] : 0.0;
-      __syncwarp();
-      if (i < m - 1) F[i + j * d] = v;
-      __syncwarp();
-    }
-  for (int i = k + lane; i < m - 1; i += 32) {
-    const int o = order[i + 1];
-    __syncwarp();
-    order[i] = o;
-  }
-  __syncwarp();
-  for (int j = 0; j < p; ++j) {  // rank-1 update of rows/columns k..m-2
-    const int jj = k + j;
-    const double ljj = F[jj + jj * d], xj = xt[j];
-    const double rr = sqrt(ljj * ljj + xj * xj);
-    const double c = rr / ljj, s = xj / ljj;
-    for (int i = j + 1 + lane; i < p; i += 32) {
-      const double lij = (F[k + i + jj * d] + s * xt[i]) / c;
-      xt[i] = c * xt[i] - s * lij;
-      F[k + i + jj * d] = lij;
-    }
-    __syncwarp();
-    if (lane == 0) F[jj + jj * d] = rr;
-    __syncwarp();
-  }
-}
-
-// z[order[a]] for L L^T z_P = q_P (forward then back substitution); y kept in zt.
-__device__ void chol_solve(const double* F, int d, const int* order, int m, const double* G, int64_t ldg, double* zt,
-                           double* z) {
-  const int lane = threadIdx.x & 31;
-  for (int a = 0; a < m; ++a) {
-    double acc = 0.0;
-    for (int b = lane; b < a; b += 32) acc += F[a + b * d] * zt[b];
-#pragma unroll
-    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) zt[a] = (G[order[a] + (int64_t)d * ldg] - acc) / F[a + a * d];
-    __syncwarp();
-  }
-  for (int a = m - 1; a >= 0; --a) {
-    double acc = 0.0;
-    for (int b = a + 1 + lane; b < m; b += 32) acc += F[b + a * d] * zt[b];
-#pragma unroll
-    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) zt[a] = (zt[a] - acc) / F[a + a * d];
-    __syncwarp();
-  }
-  for (int a = lane; a < m; a += 32) z[order[a]] = zt[a];
-  __syncwarp();
-}
-
-__global__ void __launch_bounds__(NT) k_nnls_lh(int d, const double* __restrict__ Gall, int64_t ldg, int64_t stride_g,
-                                               double* __restrict__ xall, int64_t stride_x, int32_t* __restrict__ iters,
-                                               double* __restrict__ ws, int64_t batch, int fac_in_smem) {
-  extern __shared__ __align__(16) double dsm[];
-  __shared__ NnlsSmem s;
-  const int64_t p = blockIdx.x + (int64_t)blockIdx.y * 65535;
-  if (p >= batch) return;
-  const double* __restrict__ G = Gall + p * stride_g;  // Q[i][j] = G[i + j*ldg], q[i] = G[i + d*ldg]
-  // shared: x, z, w, zt (d doubles each), order (d ints), passive / skipped (d bytes each)
-  double* x = dsm;
-  double* z = x + d;
-  double* w = z + d;
-  double* zt = w + d;
-  int* order = reinterpret_cast<int*>(zt + d);
-  unsigned char* passive = reinterpret_cast<unsigned char*>(order + d);
-  unsigned char* skipped = passive + d;
-  double* F = fac_in_smem ? dsm + NNLS_VEC_DOUBLES(d) : ws + p * (int64_t)d * d;
-  const int tid = threadIdx.x;
-
-  for (int i = tid; i < d; i += NT) {
-    x[i] = 0.0;
-    z[i] = 0.0;
-    passive[i] = 0;
-    skipped[i] = 0;
-  }
-  if (tid == 0) s.m = 0;
-  double qm = 0.0;  // tol = 1e-10 max|q|
-  for (int i = tid; i < d; i += NT) qm = fmax(qm, fabs(G[i + d * ldg]));
-  block_argmax(qm, 0, true, s);
-  const double tol = 1e-10 * fmax(s.red_v[0], 2.2250738585072014e-308);
-  const int max_iter = 30 * (d > 1 ? d : 1);
-  int it = 0;
-  int status = 0;
-  while (true) {
-    for (int i = tid; i < d; i += NT) {  // w = q - Q x (column i of G = row i of Q)
-      double acc = G[i + d * ldg];
-      for (int j = 0; j < d; ++j) acc -= G[i + j * ldg] * x[j];
-      w[i] = acc;
-    }
-    __syncthreads();
-    double bv = -INFINITY;
-    int bi = 0x7fffffff;
-    for (int i = tid; i < d; i += NT)
-      if (!passive[i] && !skipped[i] && (w[i] > bv || (w[i] == bv && i < bi))) {
-        bv = w[i];
-        bi = i;
-      }
-    block_argmax(bv, bi, bi != 0x7fffffff, s);
-    if (s.red_i[0] == 0x7fffffff || s.red_v[0] <= tol) break;
-    if (++it > max_iter) {
-      status = -1;
-      break;
-    }
-    const int t = s.red_i[0];
-    if (tid < 32) {
-      const bool ok = chol_append(F, d, order, s.m, t, G, ldg);
-      if (tid == 0) {
-        s.flag = ok ? 0 : 1;
-        if (ok) {
-          s.m += 1;
-          passive[t] = 1;
-        }
-      }
-    }
-    __syncthreads();
-    if (s.flag) {  // Q_PP not positive definite: rank-deficient passive set
-      status = -3;
-      break;
-    }
-    int inner = 0;
-    while (true) {
-      ++inner;
-      if (inner > 10 * d + 10) {
-        status = -2;
-        break;
-      }
-      if (tid < 32) chol_solve(F, d, order, s.m, G, ldg, zt, z);
-      __syncthreads();
-      const int m = s.m;
-      int bad = 0;
-      for (int a = tid; a < m; a += NT) bad |= z[order[a]] <= 0.0;
-      bad = __syncthreads_or(bad);
-      if (!bad) {
-        for (int j = tid; j < d; j += NT) {
-          x[j] = passive[j] ? z[j] : 0.0;
-          skipped[j] = 0;
-        }
-        __syncthreads();
-        break;
-      }
-      if (inner == 1 && z[t] <= 0.0) {  // degenerate entry: t is the last appended; pop it
-        if (tid == 0) {
-          passive[t] = 0;
-          skipped[t] = 1;
-          s.m -= 1;
-        }
-        __syncthreads();
-        break;
-      }
-      // step back: alpha = min over passive j with z_j <= 0 of x_j / (x_j - z_j)
-      double rv = INFINITY;
-      int ri = 0x7fffffff;
-      for (int a = tid; a < m; a += NT) {
-        const int j = order[a];
-        if (z[j] <= 0.0) {
-          const double ratio = x[j] / (x[j] - z[j]);
-          if (ratio < rv || (ratio == rv && j < ri)) {
-            rv = ratio;
-            ri = j;
-          }
-        }
-      }
-      block_argmin(rv, ri, ri != 0x7fffffff, s);
-      const double alpha = s.red_v[0];
-      const int jstar = s.red_i[0];
-      for (int j = tid; j < d; j += NT) {
-        if (!passive[j]) continue;
-        double xj = x[j] + alpha * (z[j] - x[j]);
-        if (xj <= 0.0 || j == jstar) xj = 0.0;
-        x[j] = xj;
-      }
-      __syncthreads();
-      if (tid < 32) {  // delete the dropped positions, highest first
-        int mm = s.m;
-        for (int a = mm - 1; a >= 0; --a) {
-          const int j = order[a];
-          if (x[j] == 0.0) {
-            chol_delete(F, d, order, mm, a, zt);
-            if (tid == 0) passive[j] = 0;
-            --mm;
-          }
-        }
-        if (tid == 0) s.m = mm;
-      }
-      __syncthreads();
-      if (s.m == 0) break;
-    }
-    if (status) break;
-  }
-  double* xo = xall + p * stride_x;
-  for (int j = tid; j < d; j += NT) xo[j] = x[j] < 1e-14 ? 0.0 : x[j];
-  if (tid == 0 && iters) iters[p] = status ? status : it;
-}
-
 // ---------------------------------------------------------------------------------------
-// Large d (factor does not fit in shared memory): the incremental Lawson-Hanson of
-// k_nnls_lh with the factor in the workspace ROW-major (L[a][b] at F[a*d + b], b <= a) and
+// The incremental Lawson-Hanson with the factor ROW-major (L[a][b] at F[a*d + b], b <= a) and
 // CTA-wide blocked triangular solves, so every L2 access is a coalesced row segment or a
 // 32 x 32 diagonal block held in one warp's registers: O(m^2 / 32) sequential steps per
-// solve instead of O(m^2) dependent round trips.  A deletion copies the factor into the
-// second workspace half without row/column k, then restores it with Givens rotations.
+// solve instead of O(m^2) dependent round trips.  A deletion removes row/column k (in place
+// in shared memory, else by copying into the second workspace slot), then restores the
+// trailing block with Givens rotations.
 constexpr int BK = 32;
+// x, z, w, zt, bv (d doubles each) + order (d ints) + passive, skipped (d bytes each), in doubles
+#define NNLS_BIG_VEC_DOUBLES(d) (5 * (int64_t)(d) + ((int64_t)(d) * 6 + 7) / 8 + 1)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -399,6 +158,7 @@ __device__ void big_bwd(const double* __restrict__ F, int d, int m, double* y, d
   }
 }
 
+template <bool SMEM_F>
 __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restrict__ Gall, int64_t ldg, int64_t stride_g,
                                                    double* __restrict__ xall, int64_t stride_x, int32_t* __restrict__ iters,
                                                    double* __restrict__ ws, int64_t batch) {
@@ -416,7 +176,9 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
   int* order = reinterpret_cast<int*>(bv + d);
   unsigned char* passive = reinterpret_cast<unsigned char*>(order + d);
   unsigned char* skipped = passive + d;
-  double* F = ws + p * 2 * (int64_t)d * d;  // two factor slots (deletions copy between them)
+  // factor: shared memory after the vectors (SMEM_F, d <= ~155), else two workspace slots
+  // (a deletion copies between them)
+  double* F = SMEM_F ? dsm + NNLS_BIG_VEC_DOUBLES(d) : ws + p * 2 * (int64_t)d * d;
   double* F2 = F + (int64_t)d * d;
   const int tid = threadIdx.x;
 
@@ -546,6 +308,18 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
         if (x[order[k]] != 0.0) continue;  // uniform (shared x, synchronised)
         const int mm = s.m, pp = mm - 1 - k;
         for (int i = tid; i < pp; i += NT) zt[i] = F[(size_t)(k + 1 + i) * d + k];  // old column k below k
+        if (SMEM_F) {  // in place: rows k.. take the next row without column k, one row per step
+          __syncthreads();
+          for (int i = k; i < mm - 1; ++i) {
+            double v0 = 0.0, v1 = 0.0;  // row i has i+1 <= 2 NT entries
+            const int j0 = tid, j1 = tid + NT;
+            if (j0 <= i) v0 = F[(size_t)(i + 1) * d + (j0 < k ? j0 : j0 + 1)];
+            if (j1 <= i) v1 = F[(size_t)(i + 1) * d + (j1 < k ? j1 : j1 + 1)];
+            __syncthreads();
+            if (j0 <= i) F[(size_t)i * d + j0] = v0;
+            if (j1 <= i) F[(size_t)i * d + j1] = v1;
+          }
+        } else
         for (int e = tid; e < (mm - 1) * mm / 2 + mm; e += NT) {  // copy without row/column k
           // e enumerates (i, j), j <= i < mm-1, row by row: i = floor((sqrt(8e+1)-1)/2)
           int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
@@ -562,9 +336,11 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
           for (int a = k; a < mm - 1; ++a) order[a] = order[a + 1];
           s.m = mm - 1;
         }
-        double* tmp = F;  // the copy is the factor now
-        F = F2;
-        F2 = tmp;
+        if (!SMEM_F) {  // the copy is the factor now
+          double* tmp = F;
+          F = F2;
+          F2 = tmp;
+        }
         for (int j = 0; j < pp; ++j) {  // rank-1 update L22 L22^T + x x^T of rows/columns k..mm-2
           const int jj = k + j;
           __syncthreads();  // step j-1's updates (zt, column jj-1) are visible
@@ -596,7 +372,7 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
 }  // namespace
 
 size_t nnls_smem_bytes(int64_t d, bool fac_in_smem) {
-  size_t b = (size_t)NNLS_VEC_DOUBLES(d) * sizeof(double);
+  size_t b = (size_t)NNLS_BIG_VEC_DOUBLES(d) * sizeof(double);
   if (fac_in_smem) b += (size_t)d * d * sizeof(double);
   return b;
 }
@@ -608,17 +384,17 @@ cudaError_t launch_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t 
   if (d <= 0 || batch <= 0) return cudaSuccess;
   const bool fs = nnls_factor_in_smem(d);
   const dim3 grid((unsigned)(batch < 65535 ? batch : 65535), (unsigned)((batch + 65534) / 65535));
-  if (!fs) {
-    const size_t smem = (size_t)(5 * d + (d * 6 + 15) / 8 + 1) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(k_nnls_lh_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = nnls_smem_bytes(d, fs);
+  cudaError_t e;
+  if (fs) {
+    e = cudaFuncSetAttribute(k_nnls_lh_big<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_nnls_lh_big<<<grid, NT, smem, stream>>>((int)d, G, ldg, stride_g, x, stride_x, iters, ws, batch);
-    return cudaGetLastError();
+    k_nnls_lh_big<true><<<grid, NT, smem, stream>>>((int)d, G, ldg, stride_g, x, stride_x, iters, ws, batch);
+  } else {
+    e = cudaFuncSetAttribute(k_nnls_lh_big<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_nnls_lh_big<false><<<grid, NT, smem, stream>>>((int)d, G, ldg, stride_g, x, stride_x, iters, ws, batch);
   }
-  const size_t smem = nnls_smem_bytes(d, true);
-  cudaError_t e = cudaFuncSetAttribute(k_nnls_lh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_nnls_lh<<<grid, NT, smem, stream>>>((int)d, G, ldg, stride_g, x, stride_x, iters, ws, batch, 1);
   return cudaGetLastError();
 }
 
