@@ -17,7 +17,7 @@
 //
 // One CTA (256 threads) per problem, FP64 throughout (k_nnls_lh_big): all threads for the
 // dual w = q - Q x and the argmax/argmin reductions; the factor is row-major, in shared
-// memory while it fits (d <= ~155) else in the caller's workspace, and the triangular
+// memory while it fits (d <= 157) else in the caller's workspace, and the triangular
 // solves are blocked (32-row diagonal blocks in one warp's registers, the rest CTA-wide).
 // Q is read from G (L2).
 #include <cuda_runtime.h>
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
   int* order = reinterpret_cast<int*>(bv + d);
   unsigned char* passive = reinterpret_cast<unsigned char*>(order + d);
   unsigned char* skipped = passive + d;
-  // factor: shared memory after the vectors (SMEM_F, d <= ~155), else two workspace slots
+  // factor: shared memory after the vectors (SMEM_F, d <= 157), else two workspace slots
   // (a deletion copies between them)
   double* F = SMEM_F ? dsm + NNLS_BIG_VEC_DOUBLES(d) : ws + p * 2 * (int64_t)d * d;
   double* F2 = F + (int64_t)d * d;
