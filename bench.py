@@ -323,19 +323,33 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # inputs that fit in L2 (config 1): flush L2 (256 MB write) before every step, outside
+    # the per-step events; larger inputs stream through L2 and run back to back
+    small = 4.0 * n * c <= 2 * 126e6
+    flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=device) if small else None
     with ClockSampler(local) as clk:
         _lib.check(lib.srht_profile_start(args.steps), "srht_profile_start")
-        ev0.record(stream)
-        for i in range(args.steps):
-            step()
-        ev1.record(stream)
+        pairs = []
+        if small:
+            for i in range(args.steps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                step()
+                e1.record(stream)
+                pairs.append((e0, e1))
+        else:
+            ev0.record(stream)
+            for i in range(args.steps):
+                step()
+            ev1.record(stream)
         torch.cuda.synchronize()
         kms_arr = (ctypes.c_float * args.steps)()
         kcount = ctypes.c_int()
         _lib.check(lib.srht_profile_stop(kms_arr, args.steps, ctypes.byref(kcount)), "srht_profile_stop")
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = (statistics.mean(a.elapsed_time(b) for a, b in pairs) if small else ev0.elapsed_time(ev1) / args.steps)
     kms = statistics.mean(kms_arr[i] for i in range(kcount.value))
     t = torch.tensor([ms, kms], dtype=torch.float64, device=device)
     if world > 1:
@@ -354,6 +368,29 @@ def main():
                 "peak_source": "%s (MEASURED_PEAKS.json hbm_gbs)" % peak_kind if peak_kind == "measured"
                 else "fallback 6650 GB/s (B200_PROFILING.md)",
                 "kernel_ms": kms, "share_of_step": kms / ms}
+
+    # ---- config 1: steady-state CUDA-graph replay of the step (launch bound) ----
+    graph = None
+    if small and world == 1 and not rows_mode:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device)
+        side.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream(device).wait_stream(side)
+        with torch.cuda.graph(g):
+            step()
+        reps = 200
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        graph = {"us_per_step": 1e3 * e0.elapsed_time(e1) / reps, "replays": reps,
+                 "l2": "not flushed (steady-state replay)"}
 
     # ---- e2e: the same sketch through the host-buffer C-ABI call ----
     e2e = None
@@ -374,7 +411,7 @@ def main():
             "config": {"workload": "config%d_%s" % (args.config, cfg["name"]), "n": n, "d": d, "r": r,
                        "columns": c, "input_bytes": total_in,
                        "parallelism": ("rows/%d" if rows_mode else "columns/%d") % world,
-                       "l2": "inputs larger than L2 (no flush)" if total_in > 2 * 126e6 else "flushed"},
+                       "l2": "flushed (256 MB write) before each step" if small else "inputs larger than L2 (no flush)"},
             "hbm_frac_of_measured": value / peak,
             "hbm_frac_of_8TBs": value / 8000.0,
             "roofline": roofline,
@@ -383,6 +420,8 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": args.steps * (2 if (plan_has_reduce(plan) or rows_mode) else 1),
         }
+        if graph is not None:
+            line["graph_replay"] = graph
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
