@@ -47,6 +47,14 @@ constexpr int NTHREADS = 512;
 constexpr int SIGN_OFF = NBUF * BUF_BYTES;            // per buffer: 128 threads x 16 B of D bits
 constexpr int MASK_OFF = SIGN_OFF + NBUF * 2048;
 constexpr int CTRL_OFF = MASK_OFF + V3_MAX_LOGJ * NCONS * 8;
+// Register split (per thread): producers V3_PREG, consumers V3_CREG; 256 x (P + C) <= 64K.
+#ifndef V3_PREG
+#define V3_PREG 152
+#endif
+#ifndef V3_CREG
+#define V3_CREG 96
+#endif
+static_assert(256 * (V3_PREG + V3_CREG) <= 65536, "register split");
 #ifndef V3_EMPTY_MBAR
 #define V3_EMPTY_MBAR 1
 #endif
@@ -214,6 +222,7 @@ template <int DBG>
 __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int b, unsigned char* smem) {
   Cursor c = st.cur;
   if (c.it >= P.n_items32) return;
+  const Cursor st_loaded = c;
   if ((DBG & 1) && blockIdx.x == 0 && st.f < 4096) P.trace[((size_t)2 * 4096 + st.f) * 8 + 6] = clock64();
   st.f += NBUF;
   const uint32_t bar = smem_u32(smem + CTRL_OFF + 8 * NQ * b);  // quarter q: bar + 8 q
@@ -256,7 +265,16 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
 #pragma unroll
   for (int k = 0; k < NBUF; ++k) cursor_next_active(P, c);
   st.cur = c;
-  if (c.it < P.n_items32) {
+#ifndef V3_PFD
+#define V3_PFD 3  // L2 prefetch of the tile V3_PFD active tiles beyond the one just loaded (0: none)
+#endif
+  if (V3_PFD > 0) {
+    Cursor pc = V3_PFD >= NBUF ? c : st_loaded;
+#pragma unroll
+    for (int k = 0; k < (V3_PFD >= NBUF ? V3_PFD - NBUF : V3_PFD); ++k) cursor_next_active(P, pc);
+    c = pc;
+  }
+  if (V3_PFD > 0 && c.it < P.n_items32) {
     tile_src(P, c, tile, src, full);
     if (full) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(B * 4) : "memory");
   }
@@ -304,7 +322,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
 
   if (tid < 256) {
     // =========================== producers ===========================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(V3_PREG));
     const int g = tid >> 7;
     const int p = tid & 127;
     const int n = (int)P.n;
@@ -435,7 +453,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
     }
   } else {
     // =========================== consumers ===========================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_CREG));
     const int c = tid - 256;
     const int wc = c >> 5;
     const uint32_t tbase = *tmem_slot;
