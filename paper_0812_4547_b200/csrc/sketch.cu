@@ -85,8 +85,19 @@ __device__ __forceinline__ float flip(float x, uint32_t bit) {
   return __uint_as_float(__float_as_uint(x) ^ (bit << 31));
 }
 
+// RPT = 32: the sample metadata lives in shared memory (re-read per tile, conflict-free)
+// instead of 32 registers, so the kernel fits its register budget without spilling.
+#ifndef V1_META_SMEM
+#define V1_META_SMEM 1
+#endif
+template <int RPT>
+__host__ __device__ constexpr bool meta_in_smem() { return V1_META_SMEM && RPT == 32; }
+
+#ifndef V1_THREADS_PER_SM
+#define V1_THREADS_PER_SM 512
+#endif
 template <int LOG_B, int RPT>
-__global__ void __launch_bounds__((1 << LOG_B) / 32, 512 / ((1 << LOG_B) / 32))
+__global__ void __launch_bounds__((1 << LOG_B) / 32, (meta_in_smem<RPT>() ? V1_THREADS_PER_SM : 512) / ((1 << LOG_B) / 32))
     k_sketch_tiles(const __grid_constant__ SketchParams P) {
   constexpr int B = 1 << LOG_B;
   constexpr int T = B / 32;
@@ -128,7 +139,9 @@ __global__ void __launch_bounds__((1 << LOG_B) / 32, 512 / ((1 << LOG_B) / 32))
   const int pb2 = phys(b2);
 
   // ---- sample metadata: byte offset of phys(k_lo) | k_mid << 16 ----
-  uint32_t meta[RPT];
+  constexpr bool MS = meta_in_smem<RPT>();
+  uint32_t meta[MS ? 1 : RPT];
+  uint32_t* meta_s = reinterpret_cast<uint32_t*>(tile + B);  // [RPT][T] when MS
   float acc[RPT];
   const int64_t t0 = g * (int64_t)RPT * T;
 #pragma unroll
@@ -141,7 +154,7 @@ __global__ void __launch_bounds__((1 << LOG_B) / 32, 512 / ((1 << LOG_B) / 32))
       const uint32_t mid = (uint32_t)(k >> LOG_B) & (uint32_t)(P.J - 1);
       m = ((uint32_t)phys(lo) << 2) | (mid << 16);
     }
-    meta[q] = m;
+    if constexpr (MS) meta_s[q * T + tid] = m; else meta[q] = m;
     acc[q] = 0.f;
   }
 
@@ -248,7 +261,8 @@ __global__ void __launch_bounds__((1 << LOG_B) / 32, 512 / ((1 << LOG_B) / 32))
     const char* tb = reinterpret_cast<const char*>(tile);
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-      const uint32_t m = meta[q];
+      uint32_t m;
+      if constexpr (MS) m = meta_s[q * T + tid]; else m = meta[q];
       const float z = *reinterpret_cast<const float*>(tb + (m & 0xffffu));
       acc[q] += flip(z, __popc((m >> 16) & jl) & 1u);
     }
@@ -299,7 +313,7 @@ __global__ void k_reduce_slabs(const __grid_constant__ SketchParams P, int slab_
 template <int LOG_B, int RPT>
 cudaError_t launch_t(const SketchParams& sp, int64_t items, cudaStream_t stream) {
   constexpr int B = 1 << LOG_B;
-  const size_t smem = (size_t)B * sizeof(float);
+  const size_t smem = (size_t)B * sizeof(float) + (meta_in_smem<RPT>() ? (size_t)RPT * (B / 32) * 4 : 0);
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(k_sketch_tiles<LOG_B, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
