@@ -4,31 +4,37 @@
 //   SM[t] = r^{-1/2} sum_slab (-1)^{popc(k_slab & s)} sum_j (-1)^{popc(k_mid & j)} (H_B D x_{s,j})[k_lo]
 // with B = 2^14 rows per tile.  What changes against v2:
 //
-//  * Tiles arrive by TMA bulk copy (cp.async.bulk, 64 KB per tile) into a ring of
-//    three shared-memory buffers.  Measured on B200 (profiles/r01_mb_l1_sharing.txt):
-//    a TMA fill does not take shared-memory bandwidth from LDS/STS, while an LDG
-//    stream costs ~1.3 crossbar words per word loaded.  The HBM latency also
-//    leaves the producers' critical path: the copy of tile f+3 is in flight while
-//    tiles f..f+2 are transformed and gathered.
+//  * Tiles arrive by TMA bulk copy (cp.async.bulk, four 16 KB quarters per tile, each
+//    with its own FULL mbarrier) into a ring of three shared-memory buffers, L2-prefetched
+//    three tiles ahead.  Measured on B200 (profiles/r01_mb_l1_sharing.txt): a TMA fill
+//    does not take shared-memory bandwidth from LDS/STS, while an LDG stream costs ~1.3
+//    crossbar words per word loaded.  The last consumer warp done with a buffer (its
+//    EMPTY mbarrier arrival is the one that leaves a pending count of 1) copies quarter
+//    0 and the tile's D bits; the producer thread that sees quarter 0 land copies
+//    quarters 1..3 (a lone quarter lands ~4x sooner than four concurrent ones).
 //  * Producer thread p of group g (two groups of 4 warps, alternate tiles) holds
 //    128 values.  Round 1 reads its raw rows x = e + 2p + 256h (e = 0,1; h < 64)
 //    with LDS.64 (half-warps read 32 consecutive words: conflict-free), applies D,
-//    and runs the 7 butterfly stages over row bits {0, 8..13} in registers.  After a
-//    group barrier it writes the results into the "mid" layout
+//    and runs the 7 butterfly stages over row bits {0, 8..13} in registers, quarter by
+//    quarter as the quarters land.  After a group barrier it writes the results into
+//    the "mid" layout
 //        mid(x) = col(x) + 130 row(x),  col = bits 1..7 of x,  row = bit 0 | bits 8..13 << 1
 //    (STS.32; a warp writes 32 consecutive words).  Round 2: thread p owns mid row p,
 //    reads it with LDS.64 (rows are 130 words apart, so a half-warp hits 16 distinct
 //    bank pairs), runs the stages over bits 1..7 and writes z = H_B D x back in place.
 //  * Consumer warps (8 x 32 threads, 64 accumulators each at r = 16384) gather
-//    z[k_lo] for their samples.  The packed 16-bit gather offsets live in tensor
-//    memory (TMEM, 32 KB) and are streamed per tile with tcgen05.ld, so they use no
-//    shared-memory bandwidth and no registers between tiles.  Tiles of a slab are
-//    visited in Gray-code order; the k_mid sign is carried as a frame (one
-//    conditional flip per visit, from a per-thread bit mask in shared memory).
+//    z[k_lo] for their samples.  The byte offsets of the samples' z values live in
+//    tensor memory (TMEM) and are streamed per tile with tcgen05.ld one chunk ahead, so
+//    they use no shared-memory bandwidth and no registers between tiles.  Tiles of a
+//    slab are visited in Gray-code order; the k_mid sign is carried as a frame (one
+//    conditional flip per visit, from a per-thread bit mask in shared memory).  At the
+//    end of a slab the accumulators go to the partials in slot order (coalesced);
+//    k_reduce_v3 maps slots to output rows.
 //
-// Hand-off: mbarrier FULL[b] (TMA complete, or tail tile released), named barriers
-// READY_b (z of buffer b written: 128 producer arrivals + 256 consumer syncs), GRP_g
-// (producer group), CONS (consumers; after it, consumer thread 0 refills buffer b).
+// Hand-off: mbarriers FULL[b][q] (quarter q of buffer b landed, or tail tile released)
+// and EMPTY[b] (consumer warps done with buffer b); named barriers READY_b (z of buffer
+// b written: 128 producer arrivals + 256 consumer syncs), GRP_g (producer group), CONS
+// (consumers, before TMEM is released).
 #include <cuda_runtime.h>
 
 #include "internal.cuh"
