@@ -201,12 +201,13 @@ __device__ __forceinline__ const float* col_ptr(const V3Params& P, int col) {
 }
 
 // TMA issue.  Buffer slot b (tiles f = b, b+3, ...) keeps its own cursor: the next tile to
-// load into it.  The consumer warp that finishes tile f last (shared-memory counter per
-// slot) refills the slot (measured faster than a named barrier on one refilling warp):
-// tile f+3's 64 KB of rows (L2 evict-first) plus its 2 KB of packed D bits (L2 evict-last:
-// the sign words are re-read for every column), one mbarrier transaction; then it advances
-// the slot cursor by three active tiles and prefetches that tile (f+6) into L2.
-// The cursors live in shared memory and cost the consumers no registers.
+// load into it.  The consumer warp that finishes tile f last (EMPTY[b] election; the
+// shared-memory counter is the V3_EMPTY_MBAR=0 variant) refills the slot: tile f+3's 2 KB of
+// packed D bits (L2 evict-last: the sign words are re-read for every column) and its first
+// 16 KB quarter of rows (L2 evict-first; all four quarters with V3_SPLIT_ISSUE=0, the
+// producer copies quarters 1..3 otherwise); then it advances the slot cursor by three
+// active tiles and prefetches the tile V3_PFD tiles beyond f+3 into L2.  The cursors live
+// in shared memory and cost the consumers no registers.
 struct SlotState {
   Cursor cur;   // next tile for this slot
   int count;    // consumer warps done with the slot's current tile (atomic refill)
