@@ -90,24 +90,32 @@ __global__ void k_ss_offsets(int64_t nblk, const int32_t* __restrict__ cnt, int6
   *total = acc;
 }
 
-__global__ void k_ss_write(uint64_t seed, int64_t n, int64_t d, double r, const double* __restrict__ p,
-                           const float* __restrict__ Phi, int64_t ldphi, const int64_t* __restrict__ off, int64_t cap,
-                           int32_t* __restrict__ K, float* __restrict__ out, int64_t ldout) {
+__global__ void k_ss_write(uint64_t seed, int64_t n, double r, const double* __restrict__ p,
+                           const int64_t* __restrict__ off, int64_t cap, int32_t* __restrict__ K) {
   const int64_t i0 = blockIdx.x * (int64_t)SS_CHUNK + (int64_t)threadIdx.x * SS_PER;
   const uint32_t m = chunk_mask(seed, n, r, p, i0);
   int tot;
   int64_t pos = off[blockIdx.x] + block_excl_scan_ss(__popc(m), &tot);
   for (int e = 0; e < SS_PER; ++e) {
     if ((m >> e) & 1u) {
-      if (pos < cap) {
-        const int64_t i = i0 + e;
-        const double s = 1.0 / sqrt(fmin(1.0, r * p[i]));
-        K[pos] = (int32_t)i;
-        for (int64_t j = 0; j < d; ++j) out[pos + j * ldout] = (float)((double)Phi[i + j * ldphi] * s);
-      }
+      if (pos < cap) K[pos] = (int32_t)(i0 + e);
       ++pos;
     }
   }
+}
+
+// Kept rows, scaled: 32 consecutive kept rows per CTA (lanes), warps stride over the d
+// columns, so every store instruction writes 32 consecutive output rows of one column.
+__global__ void k_ss_gather(int64_t cap, const int64_t* __restrict__ total, int64_t d, double r,
+                            const double* __restrict__ p, const float* __restrict__ Phi, int64_t ldphi,
+                            const int32_t* __restrict__ K, float* __restrict__ out, int64_t ldout) {
+  const int64_t t = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int64_t kept = *total < cap ? *total : cap;  // rows written by k_ss_write
+  if (t >= kept) return;
+  const int64_t i = K[t];
+  const double s = 1.0 / sqrt(fmin(1.0, r * p[i]));
+  for (int64_t j = threadIdx.x >> 5; j < d; j += blockDim.x >> 5)
+    out[t + j * ldout] = (float)((double)Phi[i + j * ldphi] * s);
 }
 
 }  // namespace
@@ -128,7 +136,11 @@ cudaError_t launch_subspace(int64_t n, int64_t d, int64_t r, uint64_t seed, cons
       e = cudaMemcpyAsync(kept, off + nblk, sizeof(int64_t), cudaMemcpyDeviceToHost, stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     } else {
-      k_ss_write<<<(unsigned)nblk, SS_T, 0, stream>>>(seed, n, d, (double)r, p, Phi, ldphi, off, cap, K, out, ldout);
+      k_ss_write<<<(unsigned)nblk, SS_T, 0, stream>>>(seed, n, (double)r, p, off, cap, K);
+      // rows written: min(cap, kept); the caller sized cap from the count pass
+      if (cap > 0 && d > 0)
+        k_ss_gather<<<(unsigned)((cap + 31) / 32), 256, 0, stream>>>(cap, off + nblk, d, (double)r, p, Phi, ldphi, K,
+                                                                    out, ldout);
     }
   }
   if (e == cudaSuccess) e = cudaGetLastError();
