@@ -119,6 +119,21 @@ def test_column_shards_bit_identical(lib):
     assert torch.equal(full, torch.cat(parts, dim=1))
 
 
+def test_tma_kernel_repeatable(lib):
+    # kernel v3 (TMA ring, split quarter loads, mbarrier elections, slot-order partials):
+    # repeated launches on the same input agree bit for bit, and a tail tile is included
+    import torch
+    n, c, r = (1 << 20) + 12345, 6, 8192
+    M = torch.empty((c, (n + 3) & ~3), dtype=torch.float32, device="cuda").t()[:n]  # 16-byte aligned columns
+    lib.gen_uniform(9, 0, M)
+    plan = lib.Plan(n, c - 1, r, 3)
+    ws = plan.workspace(c)
+    ref = plan.sketch_columns(M, workspace=ws).clone()
+    assert lib.library().srht_debug_last_kernel() == 3
+    for _ in range(4):
+        assert torch.equal(plan.sketch_columns(M, workspace=ws), ref)
+
+
 def test_ld_greater_than_n_and_unaligned(lib):
     import torch
     from oracle import srht as osr
