@@ -84,7 +84,7 @@ def load_traffic(config, kernel):
         return None
 
 
-KERNEL_NAMES = {1: "k_sketch_tiles", 2: "k_sketch_ws", 3: "k_sketch_tma", 4: "k_sketch_f64"}
+KERNEL_NAMES = {1: "k_sketch_tiles", 2: "k_sketch_ws", 3: "k_sketch_tma", 4: "k_sketch_f64", 5: "k_sketch_col"}
 
 
 def last_kernel(lib):
@@ -493,8 +493,13 @@ def bench_sparse(args, cfg, srht, _lib, world, rank, device):
     ms = statistics.mean(a.elapsed_time(b) for a, b in times)
     kms = statistics.mean(kms_arr[i] for i in range(kcount.value)) if kcount.value else ms
     N = plan.N
-    lb = max(10, min(14, (r - 1).bit_length()))
-    adds_per_el = lb + r / float(1 << lb)  # in-tile stages + pruned accumulate
+    kname = last_kernel(lib)
+    if kname == "k_sketch_col":  # whole-column transform: log2 N stages, no pruned accumulate
+        lb = N.bit_length() - 1
+        adds_per_el = float(lb)
+    else:
+        lb = max(10, min(14, (r - 1).bit_length()))
+        adds_per_el = lb + r / float(1 << lb)  # in-tile stages + pruned accumulate
     adds = adds_per_el * max(N, 1 << lb) * ncols
     clk_mhz = clk.summary()["sm_mhz"] or 1965.0
     alu_peak = 148 * 128 * clk_mhz * 1e6 / 1e12  # T adds/s
@@ -507,7 +512,7 @@ def bench_sparse(args, cfg, srht, _lib, world, rank, device):
                    "columns": ncols, "input_bytes": in_bytes, "output_bytes": out_bytes,
                    "l2": "flushed (256 MB write) before each step"},
         "roofline": {"bound": "alu", "achieved": adds / (kms * 1e-3) / 1e12, "peak": alu_peak, "unit": "Tadd/s",
-                     "frac": adds / (kms * 1e-3) / 1e12 / alu_peak, "traffic": None, "kernel": "k_sketch_tiles",
+                     "frac": adds / (kms * 1e-3) / 1e12 / alu_peak, "traffic": None, "kernel": kname,
                      "kernel_ms": kms, "adds_per_padded_element": adds_per_el,
                      "hbm_equiv_GBps": (in_bytes + out_bytes) / (kms * 1e-3) / 1e9},
         "clocks": clk.summary(),

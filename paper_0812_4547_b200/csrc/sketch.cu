@@ -24,6 +24,8 @@
 // exchanges in between; butterflies use packed FADD2/FFMA2 (sm_100).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace srht {
@@ -349,12 +351,120 @@ int g_kernel_force = 0;
 int g_last_kernel = 0;
 unsigned long long* g_debug_trace = nullptr;
 
+namespace {
+// ---------------------------------------------------------------------------------------
+// Whole-column kernel for N = 2^13 (config 2's batched CSC problems): one CTA of 256 threads
+// transforms a full column (8192 rows) in three register rounds of 5 + 5 + 3 bits, then
+// gathers the r kept rows of z = H_N D x.  Against the tiled kernel (8 tiles of 1024 rows,
+// one warp each, plus the pruned accumulate over the tiles) this halves the instructions
+// per column and runs 8 warps per CTA.  The tile is padded (word x at x + x/32), which
+// keeps every round's shared-memory accesses conflict-free with immediate offsets.
+constexpr int COL_N = 1 << 13, COL_T = 256;
+__device__ __forceinline__ int cpad(int x) { return x + (x >> 5); }
+
+__global__ void __launch_bounds__(COL_T) k_sketch_col(const __grid_constant__ SketchParams P) {
+  __shared__ __align__(16) float tile[COL_N + COL_N / 32];
+  const int tid = threadIdx.x;
+  const int64_t col = blockIdx.x + (int64_t)blockIdx.y * 65535;
+  if (col >= P.total_cols) return;
+  const bool second = col >= P.ncols0;
+  const ColSrc& cs = second ? P.src[1] : P.src[0];
+  const int64_t lc = second ? col - P.ncols0 : col;
+  const int64_t prob = col / P.cols_per_problem;
+  const uint32_t* __restrict__ signs = P.signs + prob * P.words32;
+  const int32_t* __restrict__ Kp = P.K + prob * P.r;
+  const int n = (int)P.n;
+  // ---- D x into the padded tile (rows >= n stay 0) ----
+  if (cs.fmt == SRHT_CSC) {
+    for (int i = tid; i < (COL_N + COL_N / 32) / 4; i += COL_T)
+      reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    const int64_t cend = cs.colptr[lc + 1];
+    for (int64_t e = cs.colptr[lc] + tid; e < cend; e += COL_T) {
+      const int row = cs.rowidx[e];
+      const uint32_t sb = (__ldg(signs + (row >> 5)) >> (row & 31)) & 1u;
+      atomicAdd(&tile[cpad(row)], flip(cs.vals[e], sb));  // duplicates are summed
+    }
+  } else {
+    const float* __restrict__ colp = cs.vals + lc * cs.ld;
+    for (int x = tid; x < COL_N; x += COL_T) {
+      const uint32_t sb = (__ldg(signs + (x >> 5)) >> (x & 31)) & 1u;
+      tile[cpad(x)] = x < n ? flip(colp[x], sb) : 0.f;
+    }
+  }
+  __syncthreads();
+  float2 v[16];
+  // ---- round A: bits 0..4 in registers; thread = bits 5..12.  x = 32 tid + u ----
+  {
+    float* base = tile + cpad(tid << 5);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = make_float2(base[2 * m], base[2 * m + 1]);
+    fwht_regs<5>(v);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      base[2 * m] = v[m].x;
+      base[2 * m + 1] = v[m].y;
+    }
+  }
+  __syncthreads();
+  // ---- round B: bits 5..9; thread = bits 0..4 | bits 10..12 << 5.  x = lane + 32 u + 1024 h ----
+  {
+    float* base = tile + cpad((tid & 31) | ((tid >> 5) << 10));
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = make_float2(base[33 * (2 * m)], base[33 * (2 * m + 1)]);
+    fwht_regs<5>(v);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      base[33 * (2 * m)] = v[m].x;
+      base[33 * (2 * m + 1)] = v[m].y;
+    }
+  }
+  __syncthreads();
+  // ---- round C: bits 10..12 (u bits 0..2) with bits 0, 1 carried along (u bits 3, 4);
+  // thread = bits 2..9.  x = f + 4 tid + 1024 g, u = g + 8 f ----
+  {
+    float* base = tile + cpad(tid << 2);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int u0 = 2 * m, u1 = 2 * m + 1;
+      v[m] = make_float2(base[(u0 >> 3) + 1056 * (u0 & 7)], base[(u1 >> 3) + 1056 * (u1 & 7)]);
+    }
+    fwht_regs<3>(v);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int u0 = 2 * m, u1 = 2 * m + 1;
+      base[(u0 >> 3) + 1056 * (u0 & 7)] = v[m].x;
+      base[(u1 >> 3) + 1056 * (u1 & 7)] = v[m].y;
+    }
+  }
+  __syncthreads();
+  // ---- the kept rows of z, scaled (coalesced stores) ----
+  float* __restrict__ o = cs.out + lc * cs.ldo;
+  for (int64_t t = tid; t < P.r; t += COL_T) o[t] = tile[cpad(Kp[t])] * P.scale;
+}
+}  // namespace
+
+// Whole-column path: N = 2^13 (the padded tile is 33 KB), one slab per column, outputs
+// written directly (no row shards).  SRHT_V1_COL=0 disables it (experiments).
+bool use_col_kernel(const srht_plan* P, const SketchParams& sp) {
+  const char* e = std::getenv("SRHT_V1_COL");
+  if (e && e[0] == '0') return false;
+  return P->N_eff == COL_N && sp.S_act == 1 && sp.s_lo == 0 && !sp.part_out && P->r <= COL_N;
+}
+
 cudaError_t launch_sketch(const srht_plan* P, const SketchParams& sp, cudaStream_t stream) {
   if (sp.total_cols <= 0) return cudaSuccess;
   const int64_t items = sp.total_cols * sp.S_act * sp.groups;
   cudaError_t e;
   const int slot = (g_prof.on && g_prof.used < g_prof.capacity) ? g_prof.used++ : -1;
   if (slot >= 0) cudaEventRecord(g_prof.ev[2 * slot], stream);
+  if (use_col_kernel(P, sp)) {
+    const int64_t zc = (sp.total_cols + 65534) / 65535;
+    k_sketch_col<<<dim3((unsigned)(sp.total_cols < 65535 ? sp.total_cols : 65535), (unsigned)zc), COL_T, 0, stream>>>(sp);
+    if (slot >= 0) cudaEventRecord(g_prof.ev[2 * slot + 1], stream);
+    g_last_kernel = 5;
+    return cudaGetLastError();
+  }
   switch (P->log_b) {
     case 10: e = launch_b<10>(P->rpt, sp, items, stream); break;
     case 11: e = launch_b<11>(P->rpt, sp, items, stream); break;

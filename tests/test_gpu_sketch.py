@@ -53,6 +53,8 @@ def check_close(got, ref, M):
     ((1 << 20) + 5 * 16384 + 1, 2, 16384, 12),  # v2: tail slab of 6 sub-blocks (inactive Gray steps)
     (1 << 14, 3, 300, 13),     # v2: a single tile
     ((1 << 14) + 1, 2, 16384, 14),  # v2: r = 16384 > n, two tiles, second holds one row
+    (5000, 3, 700, 15),        # N = 2^13: whole-column kernel, ragged n
+    (8192, 2, 8192, 16),       # N = 2^13, r = N (every row kept)
 ])
 def test_dense_random_parity(lib, n, c, r, seed):
     from oracle import srht as osr
