@@ -210,8 +210,8 @@ srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM,
  * = outer iterations, or -1 (iteration cap), -2 (inner loop cap), -3 (Q_PP not
  * positive definite).  One CTA per problem; the factor is updated
  * incrementally (append / delete with Givens rotations), in shared memory for
- * d <= 157, else in the workspace (two d x d FP64 slots per problem, row-major,
- * blocked 32-row triangular solves; srht_nnls_workspace_bytes; 0 for d <= 157),
+ * d <= 156, else in the workspace (two d x d FP64 slots per problem, row-major,
+ * blocked 32-row triangular solves; srht_nnls_workspace_bytes; 0 for d <= 156),
  * 8-byte aligned.
  * Device pointers; asynchronous on `stream`.                                  */
 size_t srht_nnls_workspace_bytes(int64_t d, int64_t batch);

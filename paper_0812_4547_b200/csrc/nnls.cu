@@ -17,7 +17,7 @@
 //
 // One CTA (256 threads) per problem, FP64 throughout (k_nnls_lh_big): all threads for the
 // dual w = q - Q x and the argmax/argmin reductions; the factor is row-major, in shared
-// memory while it fits (d <= 157) else in the caller's workspace, and the triangular
+// memory while it fits (d <= 156) else in the caller's workspace, and the triangular
 // solves are blocked (32-row diagonal blocks in one warp's registers, the rest CTA-wide).
 // Q is read from G (L2).
 #include <cuda_runtime.h>
@@ -35,6 +35,7 @@ struct NnlsSmem {
   int red_i[NT / 32];
   double alpha;
   int t, flag, m;
+  int yok;  // y = L^{-1} q_P (yv) is current for the factor
 };
 
 // Block-wide max of v over threads with ok, smallest index on ties; result in s.red_v[0] / s.red_i[0].
@@ -84,8 +85,8 @@ __device__ void block_argmin(double v, int i, bool ok, NnlsSmem& s) {
 // in shared memory, else by copying into the second workspace slot), then restores the
 // trailing block with Givens rotations.
 constexpr int BK = 32;
-// x, z, w, zt, bv (d doubles each) + order (d ints) + passive, skipped (d bytes each), in doubles
-#define NNLS_BIG_VEC_DOUBLES(d) (5 * (int64_t)(d) + ((int64_t)(d) * 6 + 7) / 8 + 1)
+// x, z, w, zt, bv, yv (d doubles each) + order (d ints) + passive, skipped (d bytes each), in doubles
+#define NNLS_BIG_VEC_DOUBLES(d) (6 * (int64_t)(d) + ((int64_t)(d) * 6 + 7) / 8 + 1)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -173,10 +174,11 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
   double* w = z + d;
   double* zt = w + d;
   double* bv = zt + d;
-  int* order = reinterpret_cast<int*>(bv + d);
+  double* yv = bv + d;  // y = L^{-1} q_P, kept across appends (one new entry per append)
+  int* order = reinterpret_cast<int*>(yv + d);
   unsigned char* passive = reinterpret_cast<unsigned char*>(order + d);
   unsigned char* skipped = passive + d;
-  // factor: shared memory after the vectors (SMEM_F, d <= 157), else two workspace slots
+  // factor: shared memory after the vectors (SMEM_F, d <= 156), else two workspace slots
   // (a deletion copies between them)
   double* F = SMEM_F ? dsm + NNLS_BIG_VEC_DOUBLES(d) : ws + p * 2 * (int64_t)d * d;
   double* F2 = F + (int64_t)d * d;
@@ -188,7 +190,10 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
     passive[i] = 0;
     skipped[i] = 0;
   }
-  if (tid == 0) s.m = 0;
+  if (tid == 0) {
+    s.m = 0;
+    s.yok = 1;
+  }
   double qm = 0.0;  // tol = 1e-10 max|q|
   for (int i = tid; i < d; i += NT) qm = fmax(qm, fabs(G[i + d * ldg]));
   block_argmax(qm, 0, true, s);
@@ -222,19 +227,31 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
       for (int a = tid; a < m; a += NT) bv[a] = G[order[a] + (int64_t)t * ldg];
       __syncthreads();
       big_fwd(F, d, m, bv, zt, part);
-      double ss = 0.0;
-      for (int a = tid; a < m; a += NT) ss += zt[a] * zt[a];
+      double ss = 0.0, sy = 0.0;  // |row|^2 and row . y (the new entry of y)
+      for (int a = tid; a < m; a += NT) {
+        ss += zt[a] * zt[a];
+        sy += zt[a] * yv[a];
+      }
       ss = warp_sum(ss);
+      sy = warp_sum(sy);
       __syncthreads();
-      if ((tid & 31) == 0) s.red_v[tid >> 5] = ss;
+      if ((tid & 31) == 0) {
+        s.red_v[tid >> 5] = ss;
+        part[tid >> 5] = sy;
+      }
       __syncthreads();
       if (tid == 0) {
-        double tot = 0.0;
-        for (int k = 0; k < NT / 32; ++k) tot += s.red_v[k];
+        double tot = 0.0, toty = 0.0;
+        for (int k = 0; k < NT / 32; ++k) {
+          tot += s.red_v[k];
+          toty += part[k];
+        }
         const double dd = G[t + (int64_t)t * ldg] - tot;
         s.flag = dd > 0.0 ? 0 : 1;
         if (dd > 0.0) {
-          F[(size_t)m * d + m] = sqrt(dd);
+          const double lmm = sqrt(dd);
+          F[(size_t)m * d + m] = lmm;
+          if (s.yok) yv[m] = (G[t + (int64_t)d * ldg] - toty) / lmm;
           order[m] = t;
           passive[t] = 1;
           s.m = m + 1;
@@ -255,9 +272,17 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
         break;
       }
       const int m = s.m;
-      for (int a = tid; a < m; a += NT) bv[a] = G[order[a] + (int64_t)d * ldg];
-      __syncthreads();
-      big_fwd(F, d, m, bv, zt, part);
+      if (s.yok) {  // forward half maintained incrementally: y = L^{-1} q_P
+        for (int a = tid; a < m; a += NT) zt[a] = yv[a];
+        __syncthreads();
+      } else {
+        for (int a = tid; a < m; a += NT) bv[a] = G[order[a] + (int64_t)d * ldg];
+        __syncthreads();
+        big_fwd(F, d, m, bv, zt, part);
+        for (int a = tid; a < m; a += NT) yv[a] = zt[a];
+        __syncthreads();
+        if (tid == 0) s.yok = 1;
+      }
       big_bwd(F, d, m, zt, bv);  // z_P (in order positions) -> bv
       for (int a = tid; a < m; a += NT) z[order[a]] = bv[a];
       __syncthreads();
@@ -335,6 +360,7 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
           passive[order[k]] = 0;
           for (int a = k; a < mm - 1; ++a) order[a] = order[a + 1];
           s.m = mm - 1;
+          s.yok = 0;  // the factor changed from row k on
         }
         if (!SMEM_F) {  // the copy is the factor now
           double* tmp = F;

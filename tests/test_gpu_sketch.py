@@ -454,7 +454,7 @@ def test_nnls_gram_matches_lawson_hanson(lib, r, d, zeros):
 
 
 def test_nnls_gram_large_d_deterministic(lib):
-    # d > 157 (factor in the workspace, CTA-wide blocked solves, deletions with Givens):
+    # d > 156 (factor in the workspace, CTA-wide blocked solves, deletions with Givens):
     # repeated runs must agree bit for bit (a race in the shared updates would not)
     import torch
     rng = np.random.default_rng(7)
