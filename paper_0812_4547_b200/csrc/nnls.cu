@@ -202,9 +202,13 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
   int it = 0;
   int status = 0;
   while (true) {
+    const int mp = s.m;
     for (int i = tid; i < d; i += NT) {  // w = q - Q x (column i of G = row i of Q)
       double acc = G[i + d * ldg];
-      for (int j = 0; j < d; ++j) acc -= G[i + j * ldg] * x[j];
+      for (int a = 0; a < mp; ++a) {  // x is zero off the passive set
+        const int j = order[a];
+        acc -= G[i + j * ldg] * x[j];
+      }
       w[i] = acc;
     }
     __syncthreads();
