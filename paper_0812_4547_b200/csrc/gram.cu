@@ -133,6 +133,93 @@ __global__ void __launch_bounds__(256) k_gram32(int64_t r, int64_t c, int64_t ba
   }
 }
 
+
+// Small c (<= 112, many problems: config 2's c = 101): one CTA per problem computes only the
+// upper triangle, as 4 x 4 register tiles (i <= j over ceil(c/4) tile rows): one thread per
+// tile, e.g. 351 threads for c = 101, 2.2x less work than 64 x 64 blocks of a padded G.
+constexpr int GTRI_K = 32;     // rows of SM staged per step
+constexpr int GTRI_PF = 12;    // staged elements per thread held in registers (next step's, prefetched)
+constexpr int GTRI_MAXC = 112;  // <= 406 tiles: 13 warps, so 128 registers per thread fit
+
+__global__ void __launch_bounds__(416) k_gram_tri(int64_t r, int64_t c, int64_t batch, const float* __restrict__ SM,
+                                                  int64_t ldsm, int64_t stride_sm, double* __restrict__ G, int64_t ldg,
+                                                  int64_t stride_g) {
+  __shared__ __align__(16) double S[GTRI_K][GTRI_MAXC + 2];  // +2: staged rows land in distinct banks
+  const int64_t p = blockIdx.x + (int64_t)blockIdx.y * 65535;
+  if (p >= batch) return;
+  const float* __restrict__ Sp = SM + p * stride_sm;
+  const int nt = (int)((c + 3) / 4), ntiles = nt * (nt + 1) / 2;
+  const int tid = threadIdx.x;
+  // this thread's tile (ti <= tj) from its linear index
+  int ti = 0, rem = tid;
+  while (ti < nt && rem >= nt - ti) {
+    rem -= nt - ti;
+    ++ti;
+  }
+  const int tj = ti + rem;
+  const bool act = tid < ntiles;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  // staging: element e = (row kk = e % 32, column cc = e / 32); a warp reads 32 consecutive rows
+  // of one column.  The next step's elements are loaded into registers during this step.
+  const int nel = GTRI_K * 4 * nt;  // including zero padding columns
+  float pf[GTRI_PF];
+#define GTRI_FETCH(K0)                                                     \
+  _Pragma("unroll") for (int u = 0; u < GTRI_PF; ++u) {                     \
+    const int e = tid + u * (int)blockDim.x;                               \
+    const int kk = e % GTRI_K, cc = e / GTRI_K;                            \
+    const int64_t k = (K0) + kk;                                           \
+    pf[u] = (e < nel && cc < c && k < r) ? Sp[k + cc * ldsm] : 0.f;        \
+  }
+  GTRI_FETCH(0)
+  for (int64_t k0 = 0; k0 < r; k0 += GTRI_K) {
+#pragma unroll
+    for (int u = 0; u < GTRI_PF; ++u) {
+      const int e = tid + u * (int)blockDim.x;
+      if (e < nel) S[e % GTRI_K][e / GTRI_K] = (double)pf[u];
+    }
+    __syncthreads();
+    if (k0 + GTRI_K < r) {
+      GTRI_FETCH(k0 + GTRI_K)
+    }
+    if (act) {
+#pragma unroll
+      for (int q = 0; q < GTRI_K; ++q) {
+        // 16-byte loads: a warp's lanes mostly share ti (broadcast) and take consecutive tj
+        const double2 a01 = *reinterpret_cast<const double2*>(&S[q][4 * ti]);
+        const double2 a23 = *reinterpret_cast<const double2*>(&S[q][4 * ti + 2]);
+        const double2 b01 = *reinterpret_cast<const double2*>(&S[q][4 * tj]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&S[q][4 * tj + 2]);
+#define GTRI_ROW(U, AU)                                                          \
+  acc[U][0] = fma(AU, b01.x, acc[U][0]);                                         \
+  acc[U][1] = fma(AU, b01.y, acc[U][1]);                                         \
+  acc[U][2] = fma(AU, b23.x, acc[U][2]);                                         \
+  acc[U][3] = fma(AU, b23.y, acc[U][3]);
+        GTRI_ROW(0, a01.x)
+        GTRI_ROW(1, a01.y)
+        GTRI_ROW(2, a23.x)
+        GTRI_ROW(3, a23.y)
+#undef GTRI_ROW
+      }
+    }
+    __syncthreads();
+  }
+  if (!act) return;
+  double* __restrict__ Gp = G + p * stride_g;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t gi = 4 * ti + u, gj = 4 * tj + v;
+      if (gi < c && gj < c && (ti != tj || gi <= gj)) {  // each element once, mirrored exactly
+        Gp[gi + gj * ldg] = acc[u][v];
+        Gp[gj + gi * ldg] = acc[u][v];
+      }
+    }
+}
 }  // namespace
 
 cudaError_t launch_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
@@ -141,6 +228,15 @@ cudaError_t launch_gram(int64_t r, int64_t c, int64_t batch, const float* SM, in
   const int nb = (int)((c + GT - 1) / GT);
   const int pairs = nb * (nb + 1) / 2;
   const int64_t zc = (batch + 65534) / 65535;
+  const int nt4 = (int)((c + 3) / 4);
+  if (c <= GTRI_MAXC && batch >= 296 &&
+      GTRI_PF * ((nt4 * (nt4 + 1) / 2 + 31) / 32 * 32) >= GTRI_K * 4 * nt4) {  // many small problems
+    const int nt = nt4, ntiles = nt * (nt + 1) / 2;
+    const int threads = ((ntiles + 31) / 32) * 32;
+    const dim3 grid((unsigned)(batch < 65535 ? batch : 65535), (unsigned)zc);
+    k_gram_tri<<<grid, threads, 0, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g);
+    return cudaGetLastError();
+  }
   if ((int64_t)pairs * batch < 296) {  // under two CTAs per SM with 64-blocks: smaller blocks
     const int nb32 = (int)((c + GT32 - 1) / GT32);
     const dim3 grid((unsigned)(nb32 * (nb32 + 1) / 2), (unsigned)(batch < 65535 ? batch : 65535), (unsigned)zc);

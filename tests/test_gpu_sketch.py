@@ -431,6 +431,21 @@ def _nnls_problem(rng, r, d, zeros):
     return SA, Sb
 
 
+@pytest.mark.parametrize("batch,c,r", [(320, 37, 100), (300, 101, 256), (296, 112, 33), (300, 128, 40), (400, 1, 50)])
+def test_gram_many_small_problems(lib, batch, c, r):
+    # batch >= 296 and c <= 128: the one-CTA-per-problem upper-triangle kernel
+    import torch
+    rng = np.random.default_rng(c)
+    SMh = rng.standard_normal((batch, c, r)).astype(np.float32)   # (batch, c, r) as sketch_batched returns
+    G = lib.gram(torch.from_numpy(SMh).cuda()).cpu().numpy()
+    S64 = SMh.astype(np.float64)
+    for p in (0, 1, batch // 2, batch - 1):
+        ref = S64[p] @ S64[p].T
+        absdot = np.abs(S64[p]) @ np.abs(S64[p]).T
+        assert np.all(np.abs(G[p] - ref) <= 1e-12 * absdot + 1e-300)
+        assert np.array_equal(G[p], G[p].T)
+
+
 @pytest.mark.parametrize("r,d,zeros", [(64, 8, 4), (512, 50, 20), (2048, 100, 50), (4096, 200, 100), (2048, 300, 150)])
 def test_nnls_gram_matches_lawson_hanson(lib, r, d, zeros):
     from oracle import nnls
