@@ -417,10 +417,10 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
     // slab) near 3% of the input, and slabs small enough to load-balance.
     const int64_t NB2 = N >> 14;
     int lj2 = 0;
-#ifndef SRHT_V3_MAX_LOGJ
-#define SRHT_V3_MAX_LOGJ 6
+#ifndef SRHT_SLAB_FACTOR
+#define SRHT_SLAB_FACTOR 64
 #endif
-    while ((int64_t(1) << lj2) < 64 * r / (1 << 14) && lj2 < SRHT_V3_MAX_LOGJ) ++lj2;
+    while ((int64_t(1) << lj2) < SRHT_SLAB_FACTOR * r / (1 << 14) && lj2 < SRHT_V3_MAX_LOGJ) ++lj2;
     while ((int64_t(1) << lj2) > NB2) --lj2;
     P->log_j2 = lj2;
     P->J2 = int64_t(1) << lj2;

@@ -114,7 +114,10 @@ extern unsigned long long* g_debug_trace;
 cudaError_t launch_sketch_ws(const srht_plan* P, const WsParams& wp, cudaStream_t stream);
 int ws_phys(int x);  // tile layout of kernel v2 (host side, for the slot layout)
 // Kernel v3 (sketch_tma.cu): dense columns with 16-byte aligned columns (TMA bulk copies).
-constexpr int V3_MAX_LOGJ = 6;
+#ifndef SRHT_V3_MAX_LOGJ
+#define SRHT_V3_MAX_LOGJ 6
+#endif
+constexpr int V3_MAX_LOGJ = SRHT_V3_MAX_LOGJ;
 struct V3Params {
   ColSrc src[2];
   int64_t ncols0, total_cols;
