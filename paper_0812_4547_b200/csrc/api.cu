@@ -379,6 +379,15 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
   int lj = 20 - lb;
   if (lj < 0) lj = 0;
   while ((int64_t(1) << lj) > NB) --lj;
+  // Few, long columns (config 3: 301 columns of 32 tiles): shorter slabs so that the
+  // (column, slab) items fill the GPU (~8 per SM; a slab reduction pass is added).
+  {
+#ifndef SRHT_V1_MIN_ITEMS
+#define SRHT_V1_MIN_ITEMS 1184
+#endif
+    const int64_t nsub = (n + P->B - 1) / P->B;
+    while (lj > 0 && batch * (d + 1) * ((nsub + (int64_t(1) << lj) - 1) >> lj) < SRHT_V1_MIN_ITEMS) --lj;
+  }
   P->log_j = lj;
   P->J = int64_t(1) << lj;
   P->n_sub = (n + P->B - 1) / P->B;
