@@ -66,6 +66,32 @@ def test_dense_random_parity(lib, n, c, r, seed):
     check_close(SM, ref, M)
 
 
+def test_random_shapes_fuzz(lib):
+    # 24 seeded random shapes across every dense path (v1 tiles, whole-column N = 2^13, v2 for
+    # unaligned ld, v3) and CSC, each checked entry by entry against the oracle
+    from oracle import srht as osr
+    rng = np.random.default_rng(2024)
+    for case in range(24):
+        n = int(rng.integers(1, 400000)) if case % 3 else int(rng.integers(4097, 8193))
+        N = 1 << max(1, (n - 1).bit_length())
+        c = int(rng.integers(1, 5))
+        r = int(rng.integers(1, min(N, 20000) + 1))
+        seed = int(rng.integers(0, 2**31))
+        M = rng.standard_normal((n, c)).astype(np.float32)
+        plan = lib.Plan(n, c - 1, r, seed)
+        if case % 4 == 1:  # CSC with ~1% density
+            mask = rng.random((n, c)) < 0.01
+            M = np.where(mask, M, 0).astype(np.float32)
+            colptr = np.concatenate([[0], np.cumsum(mask.sum(axis=0))]).astype(np.int64)
+            rowidx = np.concatenate([np.nonzero(mask[:, j])[0] for j in range(c)]).astype(np.int32)
+            vals = np.concatenate([M[mask[:, j], j] for j in range(c)]).astype(np.float32)
+            SM = plan.sketch_columns(_csc_dev(colptr, rowidx, vals, (n, c))).cpu().numpy()
+        else:
+            SM = plan.sketch_columns(to_dev(M)).cpu().numpy()
+        ref = osr.sketch(M.astype(np.float64), seed, r)
+        check_close(SM, ref, M)
+
+
 @pytest.mark.parametrize("n,r", [(4096, 256), (1 << 16, 1024), (1 << 18, 4096), (1 << 20, 16384), (50000, 1024)])
 def test_integer_inputs_bit_exact(lib, n, r):
     # Integer inputs with n * max|a| < 2^24 make every partial sum exact in FP32
