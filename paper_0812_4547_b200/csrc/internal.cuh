@@ -1,6 +1,8 @@
 // Internal declarations shared by the library's translation units.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include "../../include/srht.h"
@@ -44,6 +46,21 @@ struct srht_plan {
 };
 
 namespace srht {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) holds per device: set it once per device
+// a kernel runs on (bit per device ordinal), safely from several host threads.
+template <typename K>
+cudaError_t set_max_dyn_smem_once(K* kernel, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 
 // Plan builder (plan.cu): fills d_signs and d_K; synchronous on `stream`.
 cudaError_t build_plan_device(srht_plan* P, cudaStream_t stream);

@@ -316,13 +316,9 @@ template <int LOG_B, int RPT>
 cudaError_t launch_t(const SketchParams& sp, int64_t items, cudaStream_t stream) {
   constexpr int B = 1 << LOG_B;
   const size_t smem = (size_t)B * sizeof(float) + (meta_in_smem<RPT>() ? (size_t)RPT * (B / 32) * 4 : 0);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_sketch_tiles<LOG_B, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  const cudaError_t e = set_max_dyn_smem_once(k_sketch_tiles<LOG_B, RPT>, (int)smem, attr_done);
+  if (e != cudaSuccess) return e;
   for (int64_t done = 0; done < items;) {
     // one launch covers at most 2^31-1 items (never reached in practice)
     const int64_t cnt = items - done < 0x7fffffff ? items - done : 0x7fffffff;

@@ -196,13 +196,9 @@ __global__ void k_reduce_slabs_f64(const __grid_constant__ SketchParams P, int s
 template <int LOG_B>
 cudaError_t launch_b64(const SketchParams& sp, int64_t groups, cudaStream_t stream) {
   const size_t smem = ((size_t)1 << LOG_B) * sizeof(double);
-  static bool attr_done = false;
-  if (!attr_done) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(k_sketch_f64<LOG_B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  const cudaError_t e = set_max_dyn_smem_once(k_sketch_f64<LOG_B>, (int)smem, attr_done);
+  if (e != cudaSuccess) return e;
   const int64_t items = sp.total_cols * sp.S_act * groups;
   for (int64_t done = 0; done < items;) {
     const int64_t cnt = items - done < 0x7fffffff ? items - done : 0x7fffffff;

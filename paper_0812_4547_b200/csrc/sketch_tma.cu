@@ -598,13 +598,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
 
 template <int RPT, int DBG>
 cudaError_t launch_dbg(const V3Params& vp, int grid, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(k_sketch_tma<RPT, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  const cudaError_t e = set_max_dyn_smem_once(k_sketch_tma<RPT, DBG>, SMEM_BYTES, attr);
+  if (e != cudaSuccess) return e;
   k_sketch_tma<RPT, DBG><<<grid, NTHREADS, SMEM_BYTES, stream>>>(vp);
   return cudaGetLastError();
 }

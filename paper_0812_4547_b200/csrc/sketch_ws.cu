@@ -422,13 +422,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_ws(const __grid_constant
 template <int RPT, int DBG>
 cudaError_t launch_dbg(const WsParams& wp, int grid, cudaStream_t stream) {
   const size_t smem = 2 * (size_t)TILE_BYTES + (size_t)RPT * NCONS * 4;
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(k_sketch_ws<RPT, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  const cudaError_t e = set_max_dyn_smem_once(k_sketch_ws<RPT, DBG>, (int)smem, attr);
+  if (e != cudaSuccess) return e;
   k_sketch_ws<RPT, DBG><<<grid, NTHREADS, smem, stream>>>(wp);
   return cudaGetLastError();
 }
