@@ -545,7 +545,7 @@ def test_batched_gram_nnls_config2_shape(lib):
 
 # ---- Bernoulli keeps: sketches with the random kept count ----
 
-@pytest.mark.parametrize("n,c,r,seed", [(4096, 5, 256, 0), (1 << 20, 3, 8192, 4), (300000, 2, 2000, 7)])
+@pytest.mark.parametrize("n,c,r,seed", [(4096, 5, 256, 0), (1 << 20, 3, 8192, 4), (300000, 2, 2000, 7), (6000, 3, 800, 3)])
 def test_bernoulli_sketch_parity(lib, n, c, r, seed):
     from oracle import srht as osr
     M = np.random.default_rng(seed).standard_normal((n, c)).astype(np.float32)
