@@ -17,7 +17,15 @@ namespace srht {
 namespace {
 
 constexpr int T64 = 256;   // threads per CTA
-constexpr int RPT64 = 16;  // samples per thread per work item
+// CTAs per SM: three 64 KB tiles (B <= 2^13) fit in shared memory; occupancy beats registers here
+// (config 4: 2 CTAs / 128 registers 9.0 ms, 3 CTAs / 80 registers 7.2 ms, 1 CTA unbounded 12.0 ms)
+template <int LOG_B>
+constexpr int f64_min_blocks() { return LOG_B >= 14 ? 1 : 3; }
+#ifndef F64_RPT
+#define F64_RPT 32
+#endif
+constexpr int RPT64 = F64_RPT;  // samples per thread per work item (8192 per CTA: one pass over the
+                                // tiles serves every sample up to r = 8192)
 
 // One radix-8 pass of the unnormalized natural-order WHT over bits [bit, bit + nb) of the
 // tile index (nb <= 3): each group of 2^nb entries differing only in those bits is
@@ -53,7 +61,7 @@ __device__ __forceinline__ void wht_pass(double* tile, int bit, int nb) {
 }
 
 template <int LOG_B>
-__global__ void __launch_bounds__(T64) k_sketch_f64(const __grid_constant__ SketchParams P, int64_t groups) {
+__global__ void __launch_bounds__(T64, f64_min_blocks<LOG_B>()) k_sketch_f64(const __grid_constant__ SketchParams P, int64_t groups) {
   constexpr int B = 1 << LOG_B;
   extern __shared__ __align__(16) double tile64[];
   __shared__ int64_t s_ptr;
@@ -72,16 +80,14 @@ __global__ void __launch_bounds__(T64) k_sketch_f64(const __grid_constant__ Sket
   const uint32_t* __restrict__ signs = P.signs + prob * P.words32;
   const int32_t* __restrict__ Kp = P.K + prob * P.r;
 
-  int lo[RPT64];
-  uint32_t mid[RPT64];
+  uint32_t km[RPT64];  // k_lo | k_mid << 16 (k_lo < 2^14, k_mid < 2^16)
   double acc[RPT64];
   const int64_t t0 = g * (int64_t)RPT64 * T64;
 #pragma unroll
   for (int q = 0; q < RPT64; ++q) {
     const int64_t t = t0 + (int64_t)q * T64 + tid;
     const int32_t k = t < P.r ? Kp[t] : 0;
-    lo[q] = k & (B - 1);
-    mid[q] = (uint32_t)(k >> LOG_B) & (uint32_t)(P.J - 1);
+    km[q] = (uint32_t)(k & (B - 1)) | (((uint32_t)(k >> LOG_B) & (uint32_t)(P.J - 1)) << 16);
     acc[q] = 0.0;
   }
 
@@ -149,8 +155,8 @@ __global__ void __launch_bounds__(T64) k_sketch_f64(const __grid_constant__ Sket
     const uint32_t jl = (uint32_t)(j - j0);
 #pragma unroll
     for (int q = 0; q < RPT64; ++q) {
-      const double z = tile64[lo[q]];
-      acc[q] += (__popc(mid[q] & jl) & 1) ? -z : z;
+      const double z = tile64[km[q] & 0xffffu];
+      acc[q] += (__popc((km[q] >> 16) & jl) & 1) ? -z : z;
     }
     __syncthreads();
   }
