@@ -357,6 +357,12 @@ namespace {
 // keeps every round's shared-memory accesses conflict-free with immediate offsets.
 constexpr int COL_N = 1 << 13, COL_T = 256;
 __device__ __forceinline__ int cpad(int x) { return x + (x >> 5); }
+// Zero source for the tile fill: a bulk copy (TMA engine) instead of 264 wavefronts of STS on
+// the LSU data path, which bounds this kernel.  Device globals start zeroed.
+__device__ __align__(128) float g_col_zeros[COL_N + COL_N / 32];
+#ifndef COL_TMA_ZERO
+#define COL_TMA_ZERO 1
+#endif
 
 __global__ void __launch_bounds__(COL_T) k_sketch_col(const __grid_constant__ SketchParams P) {
   __shared__ __align__(16) float tile[COL_N + COL_N / 32];
@@ -372,9 +378,28 @@ __global__ void __launch_bounds__(COL_T) k_sketch_col(const __grid_constant__ Sk
   const int n = (int)P.n;
   // ---- D x into the padded tile (rows >= n stay 0) ----
   if (cs.fmt == SRHT_CSC) {
-    for (int i = tid; i < (COL_N + COL_N / 32) / 4; i += COL_T)
-      reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
+    if (COL_TMA_ZERO) {
+      __shared__ __align__(8) uint64_t zbar;
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&zbar);
+      if (tid == 0) {
+        constexpr uint32_t bytes = (COL_N + COL_N / 32) * 4;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(tile)),
+                     "l"(g_col_zeros), "r"(bytes), "r"(bar)
+                     : "memory");
+      }
+      __syncthreads();  // the barrier is initialised before anyone waits on it
+      asm volatile(
+          "{\n .reg .pred P;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n @!P bra W_%=;\n}" ::"r"(bar)
+          : "memory");
+    } else {
+      for (int i = tid; i < (COL_N + COL_N / 32) / 4; i += COL_T)
+        reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncthreads();
+    }
     const int64_t cend = cs.colptr[lc + 1];
     for (int64_t e = cs.colptr[lc] + tid; e < cend; e += COL_T) {
       const int row = cs.rowidx[e];
