@@ -77,6 +77,10 @@ constexpr int NQ = V3_QSPLIT ? 4 : 1;
 #define V3_SPLIT_ISSUE 1
 #endif
 constexpr bool SPLIT = V3_SPLIT_ISSUE && NQ == 4;
+#ifndef V3_REFILL_Q
+#define V3_REFILL_Q 1  // quarters copied by the refill (the producer copies the rest)
+#endif
+constexpr int NREF = SPLIT ? V3_REFILL_Q : NQ;
 // control block: FULL mbarriers [0, 8 NQ NBUF), TMEM address [96,100), EMPTY mbarriers
 // [104,128), slot states [128,..)
 constexpr int CTRL_TMEM = 96, CTRL_EMPTY = 104, CTRL_SLOTS = 128, CTRL_BYTES = 384;
@@ -239,7 +243,7 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
   tile_src(P, c, tile, src, full);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
-  for (int q = 0; q < (SPLIT ? 1 : NQ); ++q) {  // signs ride with the first part; a tail tile has no data parts
+  for (int q = 0; q < NREF; ++q) {  // signs ride with the first part; a tail tile has no data parts
     const int bytes = (full ? B * 4 / NQ : 0) + (q == 0 ? 2048 : 0);
     if (bytes)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar + 8 * q), "r"(bytes) : "memory");
@@ -262,7 +266,7 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
   if (full) {  // a tail tile is loaded by the producers themselves (guarded)
     const uint32_t dst = smem_u32(smem + (size_t)b * BUF_BYTES);
 #pragma unroll
-    for (int k = 0; k < (SPLIT ? 1 : 4); ++k)  // 16 KB each
+    for (int k = 0; k < (SPLIT ? NREF : 4); ++k)  // 16 KB each
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], 16384, [%2], %3;" ::"r"(
               dst + k * 16384),
@@ -356,7 +360,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream));
         const uint32_t dst = smem_u32(buf);
 #pragma unroll
-        for (int q = 1; q < 4; ++q) {
+        for (int q = NREF; q < 4; ++q) {
           if (full_tile) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16384;" ::"r"(fullb + 8 * q) : "memory");
             asm volatile(
