@@ -185,6 +185,20 @@ srht_status srht_sketch_rows_partial(const srht_plan* plan,
                                      void* workspace, size_t workspace_bytes,
                                      void* stream);
 
+/* Finish of a row partition (the step after the all-reduce of the partials):
+ *     SM[t + j*ldsm] = (float)(part[t + j*ldp] * r^{-1/2}),   t < r, j < cols,
+ * i.e. Algorithm 1's scale sqrt(N/r) on the normalized H_N/sqrt(N) (P:298,
+ * P:166-168), applied once in FP64 to the summed FP64 partials, then one
+ * rounding to FP32 -- the same arithmetic as the single-GPU slab reduction, so
+ * a row-sharded sketch equals srht_sketch_columns up to the FP64 association
+ * order of the partial sums.  `part` (FP64, ldp >= r) and SM (FP32, ldsm >= r)
+ * are device pointers owned by the caller; r is the plan's kept count and the
+ * scale uses the requested r (Bernoulli plans).  EINVAL on null pointers,
+ * cols < 0 or short leading dimensions.  Asynchronous on `stream`.          */
+srht_status srht_rows_finish(const srht_plan* plan, const double* part,
+                             int64_t ldp, int64_t cols, float* SM,
+                             int64_t ldsm, void* stream);
+
 /* ---- Gram matrices of sketches: the QP form of Section 3.4 ----
  * For p < batch: G_p = SM_p^T SM_p (c x c, FP64, column-major, both triangles,
  * G_p[i + j*ldg] at G + p*stride_g, ldg >= c) where SM_p is the r x c FP32

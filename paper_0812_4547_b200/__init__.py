@@ -55,6 +55,24 @@ def colmajor(x):
     return x.t().contiguous().t()
 
 
+def _check_out(out, shape, dtype, device):
+    """Raise ValueError unless `out` is a column-major `dtype` tensor of `shape` on `device`."""
+    torch = _torch()
+    if not isinstance(out, torch.Tensor) or out.dtype != dtype or out.device != torch.device(device):
+        raise ValueError("output must be a %s tensor on %s" % (dtype, device))
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError("output has shape %s, expected %s" % (tuple(out.shape), tuple(shape)))
+    rows = shape[0]
+    if len(shape) == 1:
+        if out.numel() > 1 and out.stride(0) != 1:
+            raise ValueError("vector output must be contiguous")
+        return
+    if rows > 1 and out.stride(0) != 1:
+        raise ValueError("output must be column-major (stride(0) == 1)")
+    if shape[1] > 1 and out.stride(1) < rows:
+        raise ValueError("output columns overlap (stride(1) < rows)")
+
+
 def _stream_ptr(device):
     torch = _torch()
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
@@ -166,12 +184,14 @@ class Plan:
         ws = workspace if workspace is not None else self.workspace(ncols)
         return ws.data_ptr(), int(ws.numel())
 
-    def _out(self, rows, cols, out):
+    def _out(self, rows, cols, out, dtype=None):
+        """A column-major (rows, cols) output on the plan's device: new, or the caller's after
+        checking dtype, device, shape and strides (the C ABI writes rows x cols entries)."""
         torch = _torch()
+        dtype = torch.float32 if dtype is None else dtype
         if out is None:
-            return torch.empty((cols, rows), dtype=torch.float32, device=self.device).t()
-        if out.dtype != torch.float32 or not out.is_cuda or out.stride(0) != 1:
-            raise ValueError("output must be a column-major float32 CUDA tensor")
+            return torch.empty((cols, rows), dtype=dtype, device=self.device).t()
+        _check_out(out, (rows, cols), dtype, self.device)
         return out
 
     # -- the sketch --
@@ -188,6 +208,8 @@ class Plan:
             torch = _torch()
             if Sb is None:
                 Sb = torch.empty(self.r, dtype=torch.float32, device=self.device)
+            else:
+                _check_out(Sb, (self.r,), torch.float32, self.device)
             sb_ptr = Sb.data_ptr()
         ncols = dA.cols + (1 if b is not None else 0)
         ws, wsb = self._ws_args(ncols, workspace)
@@ -221,12 +243,26 @@ class Plan:
         torch = _torch()
         keep = []
         dM = _describe(M, keep)
-        if out is None:
-            out = torch.empty((dM.cols, self.r), dtype=torch.float64, device=self.device).t()
+        out = self._out(self.r, dM.cols, out, dtype=torch.float64)
         ws, wsb = self._ws_args(dM.cols, workspace)
         ld = int(out.stride(1)) if dM.cols > 1 else self.r
         check(self._lib.srht_sketch_rows_partial(self._h, ctypes.byref(dM), int(row0), out.data_ptr(), ld, ws, wsb,
                                                  _stream_ptr(self.device)), "srht_sketch_rows_partial")
+        return out
+
+    def rows_finish(self, part, out=None):
+        """Float32 sketch r^{-1/2} * part from the summed FP64 partials of a row partition
+        (srht_rows_finish: one FP64 scale and one rounding per entry, in the library)."""
+        torch = _torch()
+        if part.dim() != 2 or part.shape[0] != self.r:
+            raise ValueError("part must be (r, c)")
+        _check_out(part, tuple(part.shape), torch.float64, self.device)
+        cols = int(part.shape[1])
+        out = self._out(self.r, cols, out)
+        ldp = int(part.stride(1)) if cols > 1 else self.r
+        ld = int(out.stride(1)) if cols > 1 else self.r
+        check(self._lib.srht_rows_finish(self._h, part.data_ptr(), ldp, cols, out.data_ptr(), ld,
+                                         _stream_ptr(self.device)), "srht_rows_finish")
         return out
 
     def sketch_batched(self, M, out=None, workspace=None):
@@ -237,6 +273,9 @@ class Plan:
         c = dM.cols // self.batch
         if out is None:
             out = torch.empty((self.batch, c, self.r), dtype=torch.float32, device=self.device)
+        elif (not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or out.device != self.device
+              or tuple(out.shape) != (self.batch, c, self.r) or not out.is_contiguous()):
+            raise ValueError("out must be a contiguous float32 (batch, c, r) tensor on %s" % self.device)
         ws, wsb = self._ws_args(dM.cols, workspace)
         check(self._lib.srht_sketch_batched(self._h, ctypes.byref(dM), out.data_ptr(), ws, wsb,
                                             _stream_ptr(self.device)), "srht_sketch_batched")

@@ -58,6 +58,7 @@ SIGNATURES = [
     ("srht_subspace_sample", ctypes.c_int, [_I64, _I64, _I64, _U64, _P, _P, _I64, _P, _P, _I64, _I64, _P]),
     ("srht_nnls_gram", ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P]),
     ("srht_sketch_rows_partial", ctypes.c_int, [_P, _MP, _I64, _P, _I64, _P, ctypes.c_size_t, _P]),
+    ("srht_rows_finish", ctypes.c_int, [_P, _P, _I64, _I64, _P, _I64, _P]),
     ("srht_status_str", ctypes.c_char_p, [ctypes.c_int]),
     ("srht_gen_uniform", ctypes.c_int, [_U64, _U64, _I64, _I64, _P, _I64, _P]),
     ("srht_profile_start", ctypes.c_int, [ctypes.c_int]),
@@ -81,9 +82,6 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    # Experiment switch: SRHT_KERNEL=v2 runs kernel v2 where kernel v3 would (A/B runs).
-    if os.environ.get("SRHT_KERNEL") == "v2":
-        lib.srht_debug_set_kernel(2)
     _lib = lib
     return lib
 

@@ -594,6 +594,16 @@ srht_status srht_sketch_rows_partial(const srht_plan* P, const srht_matrix* M, i
   return run(P, sp, ws, ws_bytes, stream, row0, M->rows);
 }
 
+srht_status srht_rows_finish(const srht_plan* P, const double* part, int64_t ldp, int64_t cols, float* SM,
+                             int64_t ldsm, void* stream) {
+  if (!P || cols < 0 || ldp < P->r || ldsm < P->r) return SRHT_EINVAL;
+  if (cols > 0 && (!part || !SM)) return SRHT_EINVAL;
+  return srht::launch_rows_finish(part, ldp, P->r, cols, 1.0 / std::sqrt((double)P->r_target), SM, ldsm,
+                                  static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
 srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
                       double* G, int64_t ldg, int64_t stride_g, void* stream) {
   if (r < 1 || c < 1 || batch < 1 || !SM || !G || ldsm < r || ldg < c) return SRHT_EINVAL;

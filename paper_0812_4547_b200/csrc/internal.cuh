@@ -173,6 +173,9 @@ cudaError_t launch_subspace(int64_t n, int64_t d, int64_t r, uint64_t seed, cons
 
 // Fixed-order slab reduction shared by every kernel.
 cudaError_t launch_reduce(const SketchParams& sp, int slab_shift, cudaStream_t stream);
+// Row-partition finish: SM = (float)(part * scale), r x cols (srht_rows_finish).
+cudaError_t launch_rows_finish(const double* part, int64_t ldp, int64_t r, int64_t cols, double scale, float* SM,
+                               int64_t ldsm, cudaStream_t stream);
 
 // Profiling (srht_profile_start/stop): event pairs around the tile kernel.
 struct ProfileState {

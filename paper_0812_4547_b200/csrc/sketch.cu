@@ -467,9 +467,23 @@ __global__ void __launch_bounds__(COL_T) k_sketch_col(const __grid_constant__ Sk
 
 // Whole-column path: N = 2^13 (the padded tile is 33 KB), one slab per column, outputs
 // written directly (no row shards).  SRHT_V1_COL=0 disables it (experiments).
+// Finish of a row partition: one FP64 scale and one rounding per entry (srht_rows_finish).
+__global__ void k_rows_finish(const double* __restrict__ part, int64_t ldp, int64_t r, int64_t cols, double scale,
+                              float* __restrict__ SM, int64_t ldsm) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+    if (t < r) SM[j * ldsm + t] = (float)(part[j * ldp + t] * scale);
+}
+
+cudaError_t launch_rows_finish(const double* part, int64_t ldp, int64_t r, int64_t cols, double scale, float* SM,
+                               int64_t ldsm, cudaStream_t stream) {
+  if (r <= 0 || cols <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)((r + 255) / 256), (unsigned)(cols < 65535 ? cols : 65535));
+  k_rows_finish<<<grid, 256, 0, stream>>>(part, ldp, r, cols, scale, SM, ldsm);
+  return cudaGetLastError();
+}
+
 bool use_col_kernel(const srht_plan* P, const SketchParams& sp) {
-  const char* e = std::getenv("SRHT_V1_COL");
-  if (e && e[0] == '0') return false;
   return P->N_eff == COL_N && sp.S_act == 1 && sp.s_lo == 0 && !sp.part_out && P->r <= COL_N;
 }
 

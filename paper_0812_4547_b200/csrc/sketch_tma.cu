@@ -477,6 +477,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
                    "r"(m4.y), "r"(m4.z), "r"(m4.w)
                    : "memory");
     }
+    // the TMEM stores must complete before the gather loads read the offsets back
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     if (c == 0) {  // slot b starts at active tile b; fill the ring, prefetch tiles 3..5
       Cursor c0;
       cursor_start(P, c0);
@@ -549,7 +551,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
                          : "r"(smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b))
                          : "memory");
             asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pend) : "l"(st));
-            if (pend == 1) tma_issue<DBG>(P, slots[b], b, smem);
+            if (pend == 1) {
+              // acquire the other warps' arrivals (their reads of buffer b) before the
+              // refill overwrites it: the phase is complete, so this wait returns at once
+              mbar_wait(smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b), (uint32_t)((f / NBUF) & 1));
+              tma_issue<DBG>(P, slots[b], b, smem);
+            }
 #else
             const int done = atomicAdd(&slots[b].count, 1);
             if (done == NCONS / 32 - 1) {

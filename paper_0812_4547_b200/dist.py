@@ -94,7 +94,8 @@ def sketch_sharded(plan, M_shard, total_cols, group=None, out=None, sketch_fn=No
     if direct:
         return out
     if total_cols % world == 0:
-        full = gathered
+        # gath_buf is cached on the plan and reused by the next call: hand out a copy
+        full = gathered if out is not None else gathered.clone()
     else:
         idx = []
         for k in range(world):
@@ -117,13 +118,15 @@ def row_range(n, world, rank, granularity):
     return min(g0 * granularity, n), min(g1 * granularity, n)
 
 
-def sketch_row_sharded(plan, M_rows, row0, group=None, partial_fn=None, workspace=None):
+def sketch_row_sharded(plan, M_rows, row0, group=None, partial_fn=None, workspace=None, finish_fn=None, out=None):
     """Sketch of a row-partitioned [A | b]: this rank's rows [row0, row0 + M_rows.rows).
 
     plan:       srht Plan (same seed on every rank)
     M_rows:     this rank's rows of every column (row_range with plan.row_shard_rows())
     partial_fn: optional replacement for ``plan.sketch_rows_partial`` with the same contract
                 (the CPU/gloo tests plug in the oracle)
+    finish_fn:  optional replacement for ``plan.rows_finish`` (r^{-1/2} scale + FP32 rounding,
+                done by the library's srht_rows_finish on the GPU path)
     Returns the float32 (r, c) sketch (column-major) on every rank.
     """
     if M_rows.shape[0] == 0:  # a rank past the last granule contributes zeros
@@ -136,4 +139,6 @@ def sketch_row_sharded(plan, M_rows, row0, group=None, partial_fn=None, workspac
         part = part.t().contiguous().t()  # column-major (r, c)
     flat = part.t()  # (c, r) view of the column-major buffer, contiguous
     dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-    return (part * (1.0 / float(plan.r) ** 0.5)).float()
+    if finish_fn is not None:
+        return finish_fn(part)
+    return plan.rows_finish(part, out=out)

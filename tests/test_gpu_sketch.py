@@ -37,31 +37,45 @@ def check_close(got, ref, M):
     return (err / np.maximum(bound, 1e-30)).max()
 
 
-@pytest.mark.parametrize("n,c,r,seed", [
-    (4096, 17, 256, 0),        # config 1 shape
-    (1000, 3, 100, 1),         # ragged tail, r not a power of two
-    (5, 2, 3, 2),              # tiny n (N = 8 < tile)
-    (1, 1, 1, 3),              # n = 1
-    (10000, 4, 350, 4),        # paper Section 4.2 shape class (n = 10,000 -> N = 16384)
-    (33333, 5, 1500, 5),       # several tiles + ragged
-    (1 << 17, 3, 4096, 6),     # multi sub-block, single slab
-    (300000, 2, 2000, 7),      # several slabs (partials + reduce)
-    (3 << 19, 2, 8192, 8),     # several slabs, B = 2^13
-    (1 << 21, 2, 16384, 9),    # B = 2^14, two slabs
-    (70000, 2, 20000, 10),     # r > 32 * threads: several sample groups
-    ((1 << 20) + 3 * 16384 + 7, 3, 8192, 11),   # v2: ragged last tile, tail slab of 4 sub-blocks
-    ((1 << 20) + 5 * 16384 + 1, 2, 16384, 12),  # v2: tail slab of 6 sub-blocks (inactive Gray steps)
-    (1 << 14, 3, 300, 13),     # v2: a single tile
-    ((1 << 14) + 1, 2, 16384, 14),  # v2: r = 16384 > n, two tiles, second holds one row
-    (5000, 3, 700, 15),        # N = 2^13: whole-column kernel, ragged n
-    (8192, 2, 8192, 16),       # N = 2^13, r = N (every row kept)
+# Tile kernel each case must run (srht_debug_last_kernel): 1 k_sketch_tiles (v1), 2 k_sketch_ws (v2,
+# dense columns not 16-byte aligned), 3 k_sketch_tma (v3, aligned dense, N >= 2^14, r <= 16384),
+# 5 k_sketch_col (whole-column kernel, N = 2^13 with enough columns for one slab per column).
+V1, V2, V3, COL = 1, 2, 3, 5
+
+
+def last_kernel(lib):
+    return lib.library().srht_debug_last_kernel()
+
+
+@pytest.mark.parametrize("n,c,r,seed,kern", [
+    (4096, 17, 256, 0, V1),         # config 1 shape
+    (1000, 3, 100, 1, V1),          # ragged tail, r not a power of two
+    (5, 2, 3, 2, V1),               # tiny n (N = 8 < tile)
+    (1, 1, 1, 3, V1),               # n = 1
+    (10000, 4, 352, 4, V3),         # paper Section 4.2 shape class (n = 10,000 -> N = 16384)
+    (33333, 5, 1500, 5, V2),        # several tiles + ragged; ld = n is not a multiple of 4
+    (1 << 17, 3, 4096, 6, V3),      # multi sub-block, single slab
+    (300000, 2, 2000, 7, V3),       # several slabs (partials + reduce)
+    (3 << 19, 2, 8192, 8, V3),      # several slabs
+    (1 << 21, 2, 16384, 9, V3),     # B = 2^14, two slabs
+    (70000, 2, 20000, 10, V1),      # r > 16384: v1 with several sample groups
+    ((1 << 20) + 3 * 16384 + 7, 3, 8192, 11, V2),   # ragged last tile, tail slab of 4 sub-blocks
+    ((1 << 20) + 5 * 16384 + 1, 2, 16384, 12, V2),  # tail slab of 6 sub-blocks (inactive Gray steps)
+    ((1 << 20) + 5 * 16384 + 4, 2, 16384, 18, V3),  # the same tail through v3 (aligned)
+    (1 << 14, 3, 300, 13, V3),      # a single tile
+    ((1 << 14) + 1, 2, 16384, 14, V2),  # r = 16384 > n, two tiles, second holds one row
+    ((1 << 14) + 4, 2, 16384, 19, V3),  # the same through v3: second tile holds 4 rows
+    (5000, 3, 700, 15, V1),         # N = 2^13, few columns: short slabs, v1
+    (8192, 2, 8192, 16, V1),        # N = 2^13, r = N (every row kept)
+    (8192, 1200, 1024, 17, COL),    # N = 2^13, many columns: whole-column kernel
 ])
-def test_dense_random_parity(lib, n, c, r, seed):
+def test_dense_random_parity(lib, n, c, r, seed, kern):
     from oracle import srht as osr
     rng = np.random.default_rng(seed)
     M = rng.standard_normal((n, c)).astype(np.float32)
     plan = lib.Plan(n, c - 1, r, seed)
     SM = plan.sketch_columns(to_dev(M)).cpu().numpy()
+    assert last_kernel(lib) == kern
     ref = osr.sketch(M.astype(np.float64), seed, r)
     check_close(SM, ref, M)
 
@@ -347,12 +361,13 @@ def _row_cuts(n, g, k):
     return [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
 
 
-@pytest.mark.parametrize("n,c,r,seed,ld_pad", [
-    ((3 << 20) + 777, 3, 8192, 21, 0),   # kernel v3 (aligned dense), ragged last shard
-    ((1 << 21) + 5, 2, 16384, 22, 1),    # ld = n + 1: kernel v2 path
-    (50000, 3, 700, 23, 0),              # small N: kernel v1 path (one slab: partials forced)
+@pytest.mark.parametrize("n,c,r,seed,ld_pad,kern", [
+    ((3 << 20) + 780, 3, 8192, 21, 0, V3),   # kernel v3 (ld = n, a multiple of 4), ragged last shard
+    ((3 << 20) + 777, 3, 8192, 24, 0, V2),   # ld = n not a multiple of 4: kernel v2
+    ((1 << 21) + 5, 2, 16384, 22, 1, V2),    # ld = n + 1: kernel v2
+    (50000, 3, 20000, 23, 0, V1),            # r > 16384: kernel v1 (partials forced)
 ])
-def test_row_shard_partials_dense(lib, n, c, r, seed, ld_pad):
+def test_row_shard_partials_dense(lib, n, c, r, seed, ld_pad, kern):
     import torch
     from oracle import srht as osr
     rng = np.random.default_rng(seed)
@@ -366,11 +381,16 @@ def test_row_shard_partials_dense(lib, n, c, r, seed, ld_pad):
     tot = np.zeros((r, c))
     for a, b in _row_cuts(n, g, 3):
         P = plan.sketch_rows_partial(Md[a:b], a, workspace=plan.workspace(c)).cpu().numpy()
+        assert last_kernel(lib) == kern
         ref = osr.sketch_rows_partial(M[a:b].astype(np.float64), a, n, seed, r)
         bound = 1e-5 * math.sqrt(n) * np.max(np.abs(M), axis=0) * math.sqrt(r)
         assert np.all(np.abs(P - ref) <= bound[None, :])
         tot += P
     scaled = (tot / math.sqrt(r)).astype(np.float32).astype(np.float64)
+    # the library's finish (srht_rows_finish) is the same FP64 scale and one rounding
+    import torch
+    fin = plan.rows_finish(torch.from_numpy(np.asfortranarray(tot)).cuda()).cpu().numpy().astype(np.float64)
+    assert np.array_equal(fin, scaled)
     # same slab partials as the full sketch; only the FP64 association order differs
     ulp = np.spacing(np.abs(full).astype(np.float32)).astype(np.float64)
     assert np.all(np.abs(scaled - full) <= ulp)
@@ -586,3 +606,37 @@ def test_subspace_uniform_equals_bernoulli_srht(lib):
     K, rows = lib.subspace_sampling(to_dev(Phi), r, torch.full((N,), 1.0 / N, dtype=torch.float64).cuda(), seed=seed)
     plan = lib.Plan(n, 1, r, seed, sampling="bernoulli")
     assert np.array_equal(K.cpu().numpy(), plan.indices())
+
+
+def test_binding_rejects_bad_outputs(lib):
+    # the C ABI writes r x c entries: wrong shape/dtype/device outputs must fail before the call
+    import torch
+    n, c, r = 20000, 3, 512
+    plan = lib.Plan(n, c - 1, r, 0)
+    M = torch.zeros((c, n), device="cuda").t()
+    bad = [torch.empty((c, r - 1), device="cuda").t(),                 # too few rows
+           torch.empty((c + 1, r), device="cuda").t(),                 # too many columns
+           torch.empty((c, r), device="cuda", dtype=torch.float64).t(),
+           torch.empty((c, r)).t(),                                     # host tensor
+           torch.empty((r, c), device="cuda")]                          # row-major
+    for out in bad:
+        with pytest.raises(ValueError):
+            plan.sketch_columns(M, out=out)
+    with pytest.raises(ValueError):
+        plan.sketch(M[:, :2], M[:, 2], Sb=torch.empty(r - 1, device="cuda"))
+    with pytest.raises(ValueError):
+        plan.sketch_rows_partial(M, 0, out=torch.empty((c, r), device="cuda").t())  # float32, not float64
+    with pytest.raises(ValueError):
+        plan.rows_finish(torch.zeros((r, c), device="cuda"))                      # float32 partials
+    bplan = lib.Plan(n, c - 1, r, 0, batch=2)
+    with pytest.raises(ValueError):
+        bplan.sketch_batched(torch.zeros((2 * c, n), device="cuda").t(), out=torch.empty((2, c, r - 1), device="cuda"))
+
+
+def test_rows_finish_invalid_arguments(lib):
+    import ctypes
+    plan = lib.Plan(1 << 16, 1, 256, 0)
+    L = lib.library()
+    assert L.srht_rows_finish(plan._h, None, 256, 1, None, 256, None) == 1       # null pointers
+    assert L.srht_rows_finish(plan._h, ctypes.c_void_p(16), 255, 1, ctypes.c_void_p(16), 256, None) == 1
+    assert L.srht_rows_finish(plan._h, None, 256, 0, None, 256, None) == 0       # nothing to do
