@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="srht", choices=["srht", "reference"])
+    ap.add_argument("--accum", default="fp32", choices=["fp32", "fp64"],
+                    help="fp32: the throughput path; fp64: the FP64-accumulation parity mode "
+                         "(DESIGN.md reading R14), which meets the 1e-6 end-to-end gate on configs 4/5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -84,7 +87,8 @@ def load_traffic(config, kernel):
         return None
 
 
-KERNEL_NAMES = {1: "k_sketch_tiles", 2: "k_sketch_ws", 3: "k_sketch_tma", 4: "k_sketch_f64", 5: "k_sketch_col"}
+KERNEL_NAMES = {1: "k_sketch_tiles", 2: "k_sketch_ws", 3: "k_sketch_tma", 4: "k_sketch_f64", 5: "k_sketch_col",
+                6: "k_sketch_tma64"}
 
 
 def last_kernel(lib):
@@ -343,7 +347,7 @@ def main():
     n, d, r, seed = cfg["n"], cfg["d"], cfg["r"], workloads.SEED
     c = d + 1
     rows_mode = args.shard == "rows"
-    plan = srht.Plan(n, d, r, seed)
+    plan = srht.Plan(n, d, r, seed, accum=args.accum)
     if rows_mode:
         # every rank holds rows [row0, row1) of all c columns (Uniform[0,1) from rank-specific
         # streams: the timing does not depend on the values)
@@ -432,11 +436,27 @@ def main():
     # read the shard once, write r x c_l (rows mode: the shard's rows, FP64 r x c partials)
     alg_bytes_launch = (4.0 * Ml.shape[0] * c + 8.0 * r * c) if rows_mode else (4.0 * n * cl + 4.0 * r * cl)
     achieved = alg_bytes_launch / (kms_max * 1e-3) / 1e9  # slowest rank's kernel
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(args.config, kname), "kernel": kname,
-                "peak_source": "%s (MEASURED_PEAKS.json hbm_gbs)" % peak_kind if peak_kind == "measured"
-                else "fallback 6650 GB/s (B200_PROFILING.md)",
-                "kernel_ms": kms_max, "share_of_step": kms_max / ms}
+    clk_now = clk.summary()
+    if args.accum == "fp64":
+        # FP64 mode: bound by the FP64 add pipe.  Algorithmic adds per padded element: log2 r + 1
+        # (SURVEY 8(d)); peak = 148 SMs x 64 FP64 lanes x the median SM clock under load
+        # (scripts/mb_dadd.cu measures the lanes).
+        lg = max(1, (r - 1).bit_length())
+        alg_adds = (lg + 1) * float(plan.N) * cl
+        clk_mhz = clk_now.get("sm_mhz") or 1965.0
+        dpeak = 148 * 64 * clk_mhz * 1e6 / 1e12
+        dach = alg_adds / (kms_max * 1e-3) / 1e12
+        roofline = {"bound": "alu", "achieved": dach, "peak": dpeak, "unit": "TFLOP/s", "frac": dach / dpeak,
+                    "traffic": None, "kernel": kname,
+                    "peak_source": "148 SMs x 64 FP64 add lanes x %.0f MHz (derived; DESIGN.md 6.1b)" % clk_mhz,
+                    "kernel_ms": kms_max, "share_of_step": kms_max / ms, "adds_per_padded_element": lg + 1,
+                    "hbm_achieved_GBps": achieved, "hbm_frac": achieved / peak}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": load_traffic(args.config, kname), "kernel": kname,
+                    "peak_source": "%s (MEASURED_PEAKS.json hbm_gbs)" % peak_kind if peak_kind == "measured"
+                    else "fallback 6650 GB/s (B200_PROFILING.md)",
+                    "kernel_ms": kms_max, "share_of_step": kms_max / ms}
 
     # ---- config 1: steady-state CUDA-graph replay of the step (launch bound) ----
     graph = None
@@ -475,8 +495,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64" if args.accum == "fp64" else "f32", "data": "synthetic",
             "config": {"workload": "config%d_%s" % (args.config, cfg["name"]), "n": n, "d": d, "r": r,
+                       "accum": args.accum,
                        "columns": c, "input_bytes": total_in,
                        "parallelism": ("rows/%d" if rows_mode else "columns/%d") % world,
                        "l2": "flushed (256 MB write) before each step" if small else "inputs larger than L2 (no flush)"},

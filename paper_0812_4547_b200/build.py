@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
          "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["plan.cu", "sketch.cu", "sketch_ws.cu", "sketch_tma.cu", "sketch_f64.cu", "gram.cu", "nnls.cu", "subspace.cu", "api.cu"]
+SOURCES = ["plan.cu", "sketch.cu", "sketch_ws.cu", "sketch_tma.cu", "sketch_f64.cu", "sketch_tma64.cu", "gram.cu", "nnls.cu", "subspace.cu", "api.cu"]
 
 
 def _compile(src, verbose):

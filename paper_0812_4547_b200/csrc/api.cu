@@ -55,8 +55,11 @@ size_t partial_bytes(const srht_plan* P, int64_t ncols, bool shards = false) {
   if (ncols <= 0) return 0;
   const int64_t min_s = shards ? 1 : 2;
   if (P->flags & SRHT_PLAN_ACCUM_FP64) {  // FP64 partials of the v1 slab geometry
-    if (P->S_act < min_s) return 0;
-    const size_t b = (size_t)P->S_act * (size_t)ncols * (size_t)P->r * sizeof(double);
+    size_t b = P->S_act < min_s ? 0 : (size_t)P->S_act * (size_t)ncols * (size_t)P->r * sizeof(double);
+    if (P->v64_ok) {  // FP64 TMA kernel: slot-order partials of every slab, even a single one
+      const size_t b64 = (size_t)P->S_act64 * P->G64 * (size_t)ncols * (size_t)P->rpt64 * 256 * sizeof(double);
+      if (b64 > b) b = b64;
+    }
     return (b + 255) & ~size_t(255);
   }
   int64_t S = P->S_act;
@@ -156,6 +159,42 @@ cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
   return e;
 }
 
+// FP64 TMA kernel: sample group gi takes samples t in [gi * slots, (gi + 1) * slots); inside a
+// group, slot (q, c) belongs to half-warp row q * 16 + c / 16, and the group's samples, sorted by
+// the 8-byte bank granule of their z value (mid(k_lo) mod 16), are dealt round-robin over the
+// rows, so the 16 lanes of a half-warp gather from distinct granules where the counts allow.
+cudaError_t build_v64_layout(srht_plan* P, const std::vector<int32_t>& K) {
+  const int rpt = P->rpt64, G = P->G64, slots = rpt * 256, rows = rpt * 16;
+  const int lj = P->log_j64 > 0 ? P->log_j64 : 1;
+  std::vector<uint32_t> meta((size_t)G * 256 * rpt, 0u);
+  std::vector<int32_t> ttab((size_t)G * 256 * rpt, -1);
+  std::vector<uint32_t> masks((size_t)G * lj * 256, 0u);
+  for (int gi = 0; gi < G; ++gi) {
+    std::vector<std::vector<int32_t>> bucket(16);
+    for (int64_t t = (int64_t)gi * slots; t < P->r && t < (int64_t)(gi + 1) * slots; ++t)
+      bucket[srht::v64_mid(K[t] & ((1 << V64_LOG_B) - 1)) & 15].push_back((int32_t)t);
+    std::vector<int> fill(rows, 0);
+    int64_t i = 0;
+    for (int bk = 0; bk < 16; ++bk)
+      for (int32_t t : bucket[bk]) {
+        const int row = (int)(i % rows);
+        const int q = row / 16, c = 16 * (row % 16) + fill[row]++;
+        ++i;
+        const int k = K[t];
+        const size_t idx = ((size_t)gi * 256 + c) * rpt + q;
+        meta[idx] = 8u * (uint32_t)srht::v64_mid(k & ((1 << V64_LOG_B) - 1));
+        ttab[idx] = t;
+        const uint32_t kmid = (uint32_t)(k >> V64_LOG_B) & (uint32_t)(P->J64 - 1);
+        for (int l = 0; l < P->log_j64; ++l)
+          if ((kmid >> l) & 1u) masks[((size_t)gi * lj + l) * 256 + c] |= 1u << q;
+      }
+  }
+  cudaError_t e = upload(&P->d_meta64, meta);
+  if (e == cudaSuccess) e = upload(&P->d_ttab64, ttab);
+  if (e == cudaSuccess) e = upload(&P->d_masks64, masks);
+  return e;
+}
+
 srht::SketchParams base_params(const srht_plan* P) {
   srht::SketchParams sp;
   std::memset(&sp, 0, sizeof(sp));
@@ -204,7 +243,48 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
   if (P->flags & SRHT_PLAN_ACCUM_FP64) {
     sp.partials64 = static_cast<double*>(ws);
     sp.partials = nullptr;
-    return srht::launch_sketch_f64(P, sp, st) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+    const bool batched1 = sp.cols_per_problem != INT64_MAX;
+    bool fast = P->v64_ok && !batched1;
+    const int nsrc = sp.total_cols > sp.ncols0 ? 2 : 1;
+    for (int i = 0; i < nsrc; ++i)
+      if (sp.src[i].ncols > 0 && !(sp.src[i].fmt == SRHT_DENSE && sp.src[i].vec)) fast = false;
+    int64_t s_lo64 = 0, S64 = 0;
+    if (fast) {
+      slab_range(row0, nrows, (int64_t(1) << V64_LOG_B) * P->J64, P->S_act64, s_lo64, S64);
+      fast = sp.total_cols * S64 * P->G64 < (int64_t(1) << 31);
+    }
+    if (!fast) return srht::launch_sketch_f64(P, sp, st) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+    srht::V64Params vp;
+    std::memset(&vp, 0, sizeof(vp));
+    vp.src[0] = sp.src[0];
+    vp.src[1] = nsrc == 2 ? sp.src[1] : srht::ColSrc();
+    vp.ncols0 = sp.ncols0;
+    vp.total_cols = sp.total_cols;
+    vp.signs = P->d_signs64;
+    vp.meta = P->d_meta64;
+    vp.masks = P->d_masks64;
+    vp.log_j = P->log_j64;
+    vp.G = P->G64;
+    vp.n = P->n;
+    vp.cols32 = (int)sp.total_cols;
+    vp.S_act32 = (int)S64;
+    vp.s_lo32 = (int)s_lo64;
+    vp.J32 = (int)P->J64;
+    vp.n_sub32 = (int)P->n_sub64;
+    vp.n_items32 = (int)(sp.total_cols * S64 * P->G64);
+    vp.partials = sp.partials64;
+    const int slot = (srht::g_prof.on && srht::g_prof.used < srht::g_prof.capacity) ? srht::g_prof.used++ : -1;
+    if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot], st);
+    cudaError_t e = srht::launch_sketch_tma64(P, vp, st);
+    if (slot >= 0) cudaEventRecord(srht::g_prof.ev[2 * slot + 1], st);
+    srht::g_last_kernel = 6;
+    if (e != cudaSuccess) return SRHT_ECUDA;
+    srht::SketchParams rp = sp;
+    rp.S_act = S64;
+    rp.s_lo = s_lo64;
+    return srht::launch_reduce64(rp, P->d_ttab64, P->rpt64, P->G64, V64_LOG_B + P->log_j64, st) == cudaSuccess
+               ? SRHT_OK
+               : SRHT_ECUDA;
   }
   const bool batched = sp.cols_per_problem != INT64_MAX;
   if (P->ws_ok && !batched) {
@@ -454,6 +534,36 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
     }
     P->v3_ok = (e == cudaSuccess) && P->log_j2 <= srht::V3_MAX_LOGJ && P->r < 0xffff;  // 16-bit t table
   }
+  // FP64 TMA kernel geometry (FP64 plans, single problem): B = 2^12, G sample groups of up to
+  // 8192 samples (32 FP64 accumulators per consumer thread), slabs of up to 512 tiles, shortened
+  // until the (group, column, slab) items give ~6 per SM.
+  if (e == cudaSuccess && (flags & SRHT_PLAN_ACCUM_FP64) && batch == 1 && N >= (int64_t(1) << V64_LOG_B) &&
+      r <= 4 * 8192) {
+    P->G64 = (int)((r + 8191) / 8192);
+    const int64_t per = (r + P->G64 - 1) / P->G64;
+    P->rpt64 = per <= 4 * 256 ? 4 : per <= 8 * 256 ? 8 : per <= 16 * 256 ? 16 : 32;
+    const int64_t n_tiles = N >> V64_LOG_B;
+    P->n_sub64 = (n + (1 << V64_LOG_B) - 1) >> V64_LOG_B;
+    int lj = 9;
+    while (lj > 0 && (int64_t(1) << lj) > n_tiles) --lj;
+    while (lj > 0 && P->G64 * (d + 1) * ((P->n_sub64 + (int64_t(1) << lj) - 1) >> lj) < 6 * 148) --lj;
+    P->log_j64 = lj;
+    P->J64 = int64_t(1) << lj;
+    P->S_act64 = (P->n_sub64 + P->J64 - 1) / P->J64;
+    std::vector<int32_t> K(r);
+    e = cudaMemcpy(K.data(), P->d_K, r * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = build_v64_layout(P, K);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_signs64, n_tiles * 64 * sizeof(uint2));
+    if (e == cudaSuccess) {
+      cudaStream_t st3;
+      e = cudaStreamCreateWithFlags(&st3, cudaStreamNonBlocking);
+      if (e == cudaSuccess) {
+        e = srht::build_v64_signs(P->d_signs, n_tiles, P->d_signs64, st3);
+        cudaStreamDestroy(st3);
+      }
+    }
+    P->v64_ok = e == cudaSuccess;
+  }
   if (e != cudaSuccess) {
     srht_plan_destroy(P);
     return e == cudaErrorMemoryAllocation ? SRHT_ENOMEM : SRHT_ECUDA;
@@ -482,6 +592,10 @@ srht_status srht_plan_destroy(srht_plan* P) {
   cudaFree(P->d_meta3);
   cudaFree(P->d_ttab3);
   cudaFree(P->d_masks3);
+  cudaFree(P->d_signs64);
+  cudaFree(P->d_meta64);
+  cudaFree(P->d_ttab64);
+  cudaFree(P->d_masks64);
   delete P;
   return SRHT_OK;
 }
@@ -564,6 +678,10 @@ int64_t srht_row_shard_rows(const srht_plan* P) {
   if (P->ws_ok) {
     const int64_t g2 = (int64_t(1) << 14) * P->J2;  // kernel v2 / v3 slab
     if (g2 > g) g = g2;
+  }
+  if (P->v64_ok) {
+    const int64_t g3 = (int64_t(1) << V64_LOG_B) * P->J64;  // FP64 TMA kernel slab
+    if (g3 > g) g = g3;
   }
   return g;  // both are powers of two, so the larger is a multiple of the smaller
 }

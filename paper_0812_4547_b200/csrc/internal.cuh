@@ -43,6 +43,16 @@ struct srht_plan {
   uint32_t* d_meta3;  // [256][rpt2/2]: two 16-bit mid-layout word offsets per word
   uint32_t* d_ttab3;  // [256][rpt2/2]: output rows t of slots (2i, 2i+1), 16 bits each (0xffff: empty)
   uint2* d_masks3;    // [log_j2][256]: bit q = bit sh of k_mid of slot (q, c)
+  // FP64-accumulation TMA kernel (sketch_tma64.cu; FP64 plans, single problem, N >= 2^12,
+  // r <= 32768): B = 2^12 tiles, slabs of J64 tiles, G64 sample groups of rpt64 * 256 slots.
+  bool v64_ok;
+  int log_j64;
+  int64_t J64, n_sub64, S_act64;
+  int rpt64, G64;
+  uint2* d_signs64;   // [N/2^12][64] D bits of rows e + 2p + 128h, bit 2(h & 15) + e of word h >> 4
+  uint32_t* d_meta64; // [G][256][rpt64]: byte offset of slot (q, c)'s z value (mid layout)
+  int32_t* d_ttab64;  // [G][256][rpt64]: output row t of the slot, -1 if empty
+  uint32_t* d_masks64;// [G][log_j64][256]: bit q = bit l of k_mid of slot (q, c)
 };
 
 namespace srht {
@@ -151,12 +161,31 @@ struct V3Params {
   int debug;                  // experiment knock-outs (srht_debug_set_mode, debug build), else 0
 };
 cudaError_t launch_sketch_tma(const srht_plan* P, const V3Params& vp, cudaStream_t stream);
+// FP64-accumulation TMA kernel (sketch_tma64.cu).
+#define V64_LOG_B 12
+struct V64Params {
+  ColSrc src[2];
+  int64_t ncols0, total_cols;
+  const uint2* signs;     // plan d_signs64
+  const uint32_t* meta;   // plan d_meta64
+  const uint32_t* masks;  // plan d_masks64
+  int log_j, G;
+  int64_t n;
+  int n_items32, cols32, S_act32, J32, n_sub32, s_lo32;  // items = G * cols * S_act (checked < 2^31)
+  double* partials;       // [S_act][G][total_cols][rpt64 * 256], slot order (k_reduce64 finishes)
+};
+cudaError_t launch_sketch_tma64(const srht_plan* P, const V64Params& vp, cudaStream_t stream);
+cudaError_t launch_reduce64(const SketchParams& sp, const int32_t* ttab, int rpt, int G, int slab_shift,
+                            cudaStream_t stream);
+int v64_mid(int x);  // kernel z layout (host side, for the slot layout)
+cudaError_t build_v64_signs(const uint64_t* signs, int64_t n_tiles, uint2* out, cudaStream_t stream);
 // Slab reduction of kernel v3's slot-order partials (sp.partials, S_act, s_lo, outputs).
 cudaError_t launch_reduce_v3(const SketchParams& sp, const uint32_t* ttab, int rpt, int slab_shift,
                              cudaStream_t stream);
 int v3_mid(int x);  // kernel-v3 z layout (host side, for the slot layout)
 extern int g_kernel_force;  // 0 auto, 2 = kernel v2 instead of v3 (srht_debug_set_kernel)
-extern int g_last_kernel;   // 1/2/3: tile kernel of the last srht_sketch* call (bench labels)
+extern int g_last_kernel;   // tile kernel of the last srht_sketch* call (bench labels): 1 tiles, 2 ws,
+                            // 3 tma, 4 f64, 5 col, 6 tma64
 // Gram matrices of sketches (gram.cu): G_p = SM_p^T SM_p in FP64.
 cudaError_t launch_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
                         double* G, int64_t ldg, int64_t stride_g, cudaStream_t stream);

@@ -336,7 +336,32 @@ __global__ void k_permute_signs_v3(const uint32_t* __restrict__ signs32, int64_t
     }
   out[idx] = make_uint4(w[0], w[1], w[2], w[3]);
 }
+// FP64 TMA kernel order: producer thread p of tile T (2^12 rows) owns rows e + 2p + 128h
+// (e < 2, h < 32); bit 2(h & 15) + e of word h >> 4.
+__global__ void k_permute_signs_v64(const uint32_t* __restrict__ signs32, int64_t n_tiles, uint2* __restrict__ out) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n_tiles * 64) return;
+  const int64_t T = idx >> 6;
+  const int p = (int)(idx & 63);
+  uint32_t w[2] = {0u, 0u};
+  for (int h = 0; h < 32; ++h)
+    for (int e = 0; e < 2; ++e) {
+      const int64_t row = (T << 12) + e + 2 * p + 128 * h;
+      const uint32_t bit = (signs32[row >> 5] >> (row & 31)) & 1u;
+      w[h >> 4] |= bit << (((h & 15) << 1) + e);
+    }
+  out[idx] = make_uint2(w[0], w[1]);
+}
 }  // namespace
+
+cudaError_t build_v64_signs(const uint64_t* signs, int64_t n_tiles, uint2* out, cudaStream_t stream) {
+  const int64_t total = n_tiles * 64;
+  k_permute_signs_v64<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(reinterpret_cast<const uint32_t*>(signs),
+                                                                           n_tiles, out);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  return e;
+}
 
 cudaError_t build_v3_signs(const uint64_t* signs, int64_t n_tiles, uint4* out, cudaStream_t stream) {
   const int64_t total = n_tiles * 128;

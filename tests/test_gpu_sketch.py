@@ -66,7 +66,7 @@ def last_kernel(lib):
     ((1 << 14) + 1, 2, 16384, 14, V2),  # r = 16384 > n, two tiles, second holds one row
     ((1 << 14) + 4, 2, 16384, 19, V3),  # the same through v3: second tile holds 4 rows
     (5000, 3, 700, 15, V1),         # N = 2^13, few columns: short slabs, v1
-    (8192, 2, 8192, 16, V1),        # N = 2^13, r = N (every row kept)
+    (8192, 2, 8192, 16, COL),       # N = 2^13, r = N: a single tile per column -> whole-column kernel
     (8192, 1200, 1024, 17, COL),    # N = 2^13, many columns: whole-column kernel
 ])
 def test_dense_random_parity(lib, n, c, r, seed, kern):
@@ -207,22 +207,81 @@ def check_fp64_mode(got, ref, M):
     assert np.all(err <= ulp + floor[None, :] + 1e-300), float((err / (ulp + floor[None, :] + 1e-300)).max())
 
 
-@pytest.mark.parametrize("n,c,r,seed", [
-    (4096, 17, 256, 0),        # config 1 shape
-    (1000, 3, 100, 1),         # ragged, r not a power of two
-    (1, 1, 1, 3),              # n = 1
-    (300000, 2, 2000, 7),      # several slabs: FP64 partials + FP64 reduce
-    (1 << 21, 2, 16384, 9),    # B = 2^14, two slabs
-    (70000, 2, 20000, 10),     # several sample groups
+F64, TMA64 = 4, 6  # k_sketch_f64 (CSC, batched, small or unaligned inputs), k_sketch_tma64 (aligned dense)
+
+
+@pytest.mark.parametrize("n,c,r,seed,kern", [
+    (4096, 17, 256, 0, TMA64),        # config 1 shape: a single 2^12 tile
+    (1000, 3, 100, 1, F64),           # N < 2^12: the plain FP64 kernel
+    (1, 1, 1, 3, F64),                # n = 1
+    (33333, 3, 1500, 5, F64),         # ld = n not a multiple of 4 (no TMA)
+    (300000, 2, 2000, 7, TMA64),      # several slabs: FP64 partials + FP64 reduce
+    (5000, 3, 700, 15, TMA64),        # ragged tail tile (904 rows) staged by the producers
+    ((1 << 20) + 4100, 2, 8192, 11, TMA64),  # tail tile of 4 rows, last slab short
+    (3 << 19, 3, 8192, 8, TMA64),     # r = 8192: one sample group of 32 accumulators per thread
+    (1 << 21, 2, 16384, 9, TMA64),    # two sample groups
+    (70000, 2, 20000, 10, TMA64),     # three sample groups, r not a multiple of the group size
+    (40000, 2, 30000, 12, TMA64),     # four sample groups
+    (1 << 16, 2, 37, 13, TMA64),      # 4 accumulators per thread, most slots empty
+    (70000, 2, 40000, 14, F64),       # r > 32768: the plain FP64 kernel
 ])
-def test_fp64_mode_dense_parity(lib, n, c, r, seed):
+def test_fp64_mode_dense_parity(lib, n, c, r, seed, kern):
     from oracle import srht as osr
     rng = np.random.default_rng(seed)
     M = rng.standard_normal((n, c)).astype(np.float32)
     plan = lib.Plan(n, c - 1, r, seed, accum="fp64")
     SM = plan.sketch_columns(to_dev(M), workspace=plan.workspace(c)).cpu().numpy()
+    assert last_kernel(lib) == kern
     ref = osr.sketch(M.astype(np.float64), seed, r)
     check_fp64_mode(SM, ref, M)
+
+
+@pytest.mark.parametrize("n,r", [(1 << 20, 4096), (3 << 18, 16384), (50000, 1024), (4096, 64)])
+def test_fp64_mode_integer_inputs_correctly_rounded(lib, n, r):
+    # Integers up to 2^24 are exact in FP32 and their sums (< 2^53) exact in FP64 under any
+    # order; r = 4^j makes the scale a power of two.  So the FP64 mode must return the exact
+    # sketch rounded once to FP32 -- the oracle's value rounded to FP32, bit for bit.
+    from oracle import srht as osr
+    rng = np.random.default_rng(n + r)
+    M = rng.integers(-(1 << 24), (1 << 24) + 1, size=(n, 3)).astype(np.float32)
+    plan = lib.Plan(n, 2, r, 17, accum="fp64")
+    SM = plan.sketch_columns(to_dev(M), workspace=plan.workspace(3)).cpu().numpy()
+    assert last_kernel(lib) == TMA64
+    ref = osr.sketch(M.astype(np.float64), 17, r).astype(np.float32)
+    assert np.array_equal(SM, ref)
+
+
+def test_fp64_mode_repeatable_and_shard_invariant(lib):
+    # deterministic (fixed slab order) and independent of how the columns are split
+    import torch
+    n, c, r = (1 << 20) + 4100, 6, 8192
+    M = to_dev(np.random.default_rng(5).random((n, c), dtype=np.float32))
+    plan = lib.Plan(n, c - 1, r, 3, accum="fp64")
+    ws = plan.workspace(c)
+    a = plan.sketch_columns(M, workspace=ws).clone()
+    b = plan.sketch_columns(M, workspace=ws)
+    assert torch.equal(a, b)
+    parts = torch.cat([plan.sketch_columns(M[:, :2], workspace=ws), plan.sketch_columns(M[:, 2:], workspace=ws)], 1)
+    assert torch.equal(a, parts)
+
+
+def test_fp64_mode_row_shards_dense(lib):
+    import torch
+    from oracle import srht as osr
+    n, c, r, seed = (3 << 19) + 780, 3, 16384, 31
+    M = np.random.default_rng(seed).standard_normal((n, c)).astype(np.float32)
+    Md = to_dev(M)
+    plan = lib.Plan(n, c - 1, r, seed, accum="fp64")
+    g = plan.row_shard_rows()
+    tot = np.zeros((r, c))
+    for a, b in _row_cuts(n, g, 3):
+        P = plan.sketch_rows_partial(Md[a:b], a, workspace=plan.workspace(c)).cpu().numpy()
+        assert last_kernel(lib) == TMA64
+        ref = osr.sketch_rows_partial(M[a:b].astype(np.float64), a, n, seed, r)
+        assert np.all(np.abs(P - ref) <= 1e-9 * np.maximum(np.abs(ref), 1.0))
+        tot += P
+    fin = plan.rows_finish(torch.from_numpy(np.asfortranarray(tot)).cuda()).cpu().numpy()
+    check_fp64_mode(fin, osr.sketch(M.astype(np.float64), seed, r), M)
 
 
 def test_fp64_mode_csc_and_batched(lib):
