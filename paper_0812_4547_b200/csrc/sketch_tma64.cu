@@ -10,14 +10,17 @@
 // dense 16-byte aligned columns (k_sketch_f64 in sketch_f64.cu still serves CSC, batched and
 // small inputs).  Structure, the FP64 counterpart of kernel v3:
 //
-//  * B = 2^12 rows per tile: the raw FP32 tile (16 KB) and its 512 B of packed D bits arrive by
-//    TMA bulk copy into a ring of six 33 KB buffers; the last consumer warp done with a buffer
-//    refills it (EMPTY mbarrier election, acquire wait, then the copy), and the tile after the
-//    next ring turn is prefetched into L2.
+//  * B = 2^12 rows per tile.  The raw FP32 tile (16 KB) and its 512 B of packed D bits arrive by
+//    TMA bulk copy into a ring of five raw slots, separate from the z buffers: the producer group
+//    that has read a slot (round 1) refills it with the tile five ahead at once, so loads run a
+//    whole production time ahead (a ring shared with the z buffers, refilled only when the
+//    consumers are done with a tile, left the producers waiting on the loads: 2.0 ms on config 4).
+//    The tile three beyond the next ring turn is prefetched into L2.
 //  * Four producer groups of 64 threads (two warps) take the tiles in turn.  Thread p holds 64
 //    doubles.  Round 1: rows x = e + 2p + 128h (e < 2, h < 32) read as float2 (a warp reads
 //    256 consecutive bytes), D applied by XOR on the FP32 sign bit, widened to FP64, 6 butterfly
-//    stages over row bits {0, 7..11}; stored into the mid layout
+//    stages over row bits {0, 7..11}; stored into the group's own z buffer (once the consumers
+//    are done with its previous tile: ZEMPTY mbarrier) in the mid layout
 //        mid(x) = ((x >> 1) & 63) + 66 * ((x & 1) | ((x >> 7) << 1))   (doubles)
 //    (a warp stores 32 consecutive doubles).  Round 2: thread p owns mid row p (64 doubles,
 //    double2 loads; rows are 528 B apart, so 8 threads of a quarter-warp hit 8 distinct 16-byte
@@ -40,16 +43,19 @@ namespace v64 {
 constexpr int LOG_B = V64_LOG_B;
 constexpr int B = 1 << LOG_B;
 constexpr int ROW = 66;                       // mid-layout row stride in doubles
-constexpr int BUF_BYTES = 64 * ROW * 8;       // 33792 (raw tile needs 16384)
-constexpr int NBUF = 6;
+constexpr int Z_BYTES = 64 * ROW * 8;         // 33792: one z (mid-layout) buffer per producer group
 constexpr int NGRP = 4;                       // producer groups of 64 threads
+constexpr int NRAW = 5;                       // raw-tile ring (FP32 rows + D bits, TMA-filled)
+constexpr int RAW_BYTES = B * 4;              // 16384
+constexpr int SIGN_BYTES = 512;               // 64 threads x 64 bits of D per tile
+constexpr int RAWSLOT = RAW_BYTES + SIGN_BYTES;
 constexpr int NPROD = NGRP * 64;
 constexpr int NCONS = 256;
 constexpr int NTHREADS = NPROD + NCONS;
-constexpr int SIGN_BYTES = 512;               // 64 threads x 64 bits of D per tile
-constexpr int SIGN_OFF = NBUF * BUF_BYTES;
-constexpr int CTRL_OFF = SIGN_OFF + NBUF * SIGN_BYTES;
-constexpr int CTRL_FULL = 0, CTRL_EMPTY = 64, CTRL_TMEM = 128, CTRL_SLOTS = 144, CTRL_BYTES = 448;
+constexpr int RAW_OFF = NGRP * Z_BYTES;       // 135168
+constexpr int CTRL_OFF = RAW_OFF + NRAW * RAWSLOT;
+// control block: FULL[raw slot] mbarriers, ZEMPTY[group] mbarriers, TMEM address
+constexpr int CTRL_FULL = 0, CTRL_ZEMPTY = 64, CTRL_TMEM = 128, CTRL_BYTES = 256;
 constexpr int SMEM_BYTES = CTRL_OFF + CTRL_BYTES;
 static_assert(SMEM_BYTES <= 232448, "shared memory");
 #ifndef V64_PREG
@@ -60,10 +66,10 @@ static_assert(SMEM_BYTES <= 232448, "shared memory");
 #endif
 static_assert(NPROD * V64_PREG + NCONS * V64_CREG <= 65536, "register split");
 #ifndef V64_PFD
-#define V64_PFD 2  // L2 prefetch of the tile this many active tiles beyond the one just loaded
+#define V64_PFD 3  // L2 prefetch of the tile this many active tiles beyond the one just loaded
 #endif
 
-enum { BAR_READY0 = 1, BAR_GRP0 = BAR_READY0 + NBUF, BAR_CONS = BAR_GRP0 + NGRP };  // 0 = __syncthreads
+enum { BAR_READY0 = 1, BAR_GRP0 = BAR_READY0 + NGRP, BAR_CONS = BAR_GRP0 + NGRP };  // 0 = __syncthreads
 static_assert(BAR_CONS < 16, "named barriers");
 
 __host__ __device__ constexpr int mid(int x) { return ((x >> 1) & 63) + ROW * ((x & 1) | ((x >> 7) << 1)); }
@@ -120,10 +126,6 @@ __device__ __forceinline__ void fwht64(double (&v)[64]) {
 struct Cursor {
   int it, pp, np, cnt, s, col, gi;
 };
-struct SlotState {
-  Cursor cur;  // next tile to load into this buffer slot
-};
-static_assert(CTRL_SLOTS + NBUF * (int)sizeof(SlotState) <= CTRL_BYTES, "control block overflows");
 
 __device__ __forceinline__ int gray(int pp) { return pp ^ (pp >> 1); }
 __device__ __forceinline__ void cursor_item(const V64Params& P, Cursor& c) {
@@ -161,44 +163,42 @@ __device__ __forceinline__ const float* col_ptr(const V64Params& P, int col) {
   return base + lc * ld;
 }
 
-// Refill buffer slot b with the slot's next tile (its D bits, and its rows unless it is the
-// ragged tail tile, which the producers stage themselves), advance the slot cursor by one ring
-// turn, and prefetch a later tile into L2.
-__device__ __forceinline__ void tma_issue(const V64Params& P, SlotState& st, int b, unsigned char* smem) {
-  Cursor c = st.cur;
+// Load tile `c` into raw slot k (its D bits, and its rows unless it is the ragged tail tile,
+// which the producers stage themselves), then prefetch the tile V64_PFD active tiles beyond the
+// next ring turn into L2.
+__device__ __forceinline__ void raw_issue(const V64Params& P, Cursor c, int k, unsigned char* smem) {
   if (c.it >= P.n_items32) return;
-  const uint32_t bar = smem_u32(smem + CTRL_OFF + CTRL_FULL + 8 * b);
+  const uint32_t bar = smem_u32(smem + CTRL_OFF + CTRL_FULL + 8 * k);
   const int tile = c.s * P.J32 + gray(c.pp);
   const int64_t row0 = (int64_t)tile * B;
   const bool full = row0 + B <= P.n;
-  const float* src = col_ptr(P, c.col) + row0;
+  unsigned char* slot = smem + RAW_OFF + (size_t)k * RAWSLOT;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-               "r"((full ? B * 4 : 0) + SIGN_BYTES)
+               "r"((full ? RAW_BYTES : 0) + SIGN_BYTES)
                : "memory");
   uint64_t keep, stream;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream));
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(smem + SIGN_OFF + SIGN_BYTES * b)),
+          smem_u32(slot + RAW_BYTES)),
       "l"(P.signs + (int64_t)tile * 64), "n"(SIGN_BYTES), "r"(bar), "l"(keep)
       : "memory");
   if (full)
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(smem + (size_t)b * BUF_BYTES)),
-        "l"(src), "n"(B * 4), "r"(bar), "l"(stream)
+            smem_u32(slot)),
+        "l"(col_ptr(P, c.col) + row0), "n"(RAW_BYTES), "r"(bar), "l"(stream)
         : "memory");
-#pragma unroll
-  for (int k = 0; k < NBUF; ++k) cursor_next_active(P, c);
-  st.cur = c;
   if (V64_PFD > 0) {
-#pragma unroll
-    for (int k = 0; k < V64_PFD; ++k) cursor_next_active(P, c);
+#pragma unroll 1
+    for (int i = 0; i < NRAW + V64_PFD; ++i) cursor_next_active(P, c);
     if (c.it < P.n_items32) {
       const int64_t r1 = (int64_t)(c.s * P.J32 + gray(c.pp)) * B;
-      if (r1 + B <= P.n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(col_ptr(P, c.col) + r1), "n"(B * 4) : "memory");
+      if (r1 + B <= P.n)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(col_ptr(P, c.col) + r1), "n"(RAW_BYTES)
+                     : "memory");
     }
   }
 }
@@ -207,17 +207,16 @@ template <int RPT>
 __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma64(const __grid_constant__ V64Params P) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + CTRL_TMEM);
-  SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + CTRL_SLOTS);
   const int tid = threadIdx.x;
   const int MWT = P.G * RPT;  // TMEM columns per consumer warp half (offsets of every group)
   const int tcols = (2 * MWT) <= 32 ? 32 : (2 * MWT) <= 64 ? 64 : (2 * MWT) <= 128 ? 128 : 256;
 
   if (tid == 0) {
-    for (int b = 0; b < NBUF; ++b) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(smem + CTRL_OFF + CTRL_FULL + 8 * b)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b)),
+    for (int k = 0; k < NRAW; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(smem + CTRL_OFF + CTRL_FULL + 8 * k)));
+    for (int g = 0; g < NGRP; ++g)  // ZEMPTY[g]: one arrival per consumer warp
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(smem + CTRL_OFF + CTRL_ZEMPTY + 8 * g)),
                    "r"(NCONS / 32));
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid >= NPROD && tid < NPROD + 32) {  // consumer warp 0 allocates TMEM
@@ -237,16 +236,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma64(const __grid_const
     const int64_t n = P.n;
     Cursor cur;
     cursor_start(P, cur);
+    if (tid == 0) {  // fill the raw ring: flat tiles 0 .. NRAW-1
+      Cursor c0 = cur;
+      for (int k = 0; k < NRAW; ++k) {
+        raw_issue(P, c0, k, smem);
+        cursor_next_active(P, c0);
+      }
+    }
     for (int k = 0; k < g; ++k) cursor_next_active(P, cur);
     int f = g;
+    double* zb = reinterpret_cast<double*>(smem + (size_t)g * Z_BYTES);
+    const uint32_t zempty = smem_u32(smem + CTRL_OFF + CTRL_ZEMPTY + 8 * g);
     while (cur.it < P.n_items32) {
-      const int b = f % NBUF;
-      const uint32_t parity = (uint32_t)((f / NBUF) & 1);
+      const int k = f % NRAW;
       const int64_t row0 = (int64_t)(cur.s * P.J32 + gray(cur.pp)) * B;
-      float* raw = reinterpret_cast<float*>(smem + (size_t)b * BUF_BYTES);
-      double* buf = reinterpret_cast<double*>(smem + (size_t)b * BUF_BYTES);
-      mbar_wait(smem_u32(smem + CTRL_OFF + CTRL_FULL + 8 * b), parity);
-      const uint2 sg = *reinterpret_cast<const uint2*>(smem + SIGN_OFF + SIGN_BYTES * b + 8 * p);
+      unsigned char* slot = smem + RAW_OFF + (size_t)k * RAWSLOT;
+      float* raw = reinterpret_cast<float*>(slot);
+      mbar_wait(smem_u32(smem + CTRL_OFF + CTRL_FULL + 8 * k), (uint32_t)((f / NRAW) & 1));
+      const uint2 sg = *reinterpret_cast<const uint2*>(slot + RAW_BYTES + 8 * p);
       if (row0 + B > n) {  // ragged tail tile (no TMA data): stage it, rows >= n read as zero
         const float* colp = col_ptr(P, cur.col);
 #pragma unroll 4
@@ -267,13 +274,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma64(const __grid_const
         v[2 * h] = (double)flipf(x.x, __funnelshift_l(w, w, 31 - bt) & 0x80000000u);
         v[2 * h + 1] = (double)flipf(x.y, __funnelshift_l(w, w, 30 - bt) & 0x80000000u);
       }
+      bar_sync(BAR_GRP0 + g, 64);  // every raw row of slot k has been read: refill it (tile f + NRAW)
+      if (p == 0) {
+        Cursor cn = cur;
+#pragma unroll 1
+        for (int i = 0; i < NRAW; ++i) cursor_next_active(P, cn);
+        raw_issue(P, cn, k, smem);
+      }
       fwht64(v);  // row bits 0 and 7..11
-      bar_sync(BAR_GRP0 + g, 64);  // every raw row of the tile has been read
+      if (f >= NGRP) mbar_wait(zempty, (uint32_t)(((f / NGRP) - 1) & 1));  // consumers done with tile f - 4
 #pragma unroll
-      for (int u = 0; u < 64; ++u) buf[p + ROW * u] = v[u];
+      for (int u = 0; u < 64; ++u) zb[p + ROW * u] = v[u];
       bar_sync(BAR_GRP0 + g, 64);
       // ---- round 2: mid row p (row bits 1..6 in registers) ----
-      double* rowp = buf + ROW * p;
+      double* rowp = zb + ROW * p;
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const double2 d2 = *reinterpret_cast<const double2*>(rowp + 2 * m);
@@ -283,9 +297,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma64(const __grid_const
       fwht64(v);
 #pragma unroll
       for (int m = 0; m < 32; ++m) *reinterpret_cast<double2*>(rowp + 2 * m) = make_double2(v[2 * m], v[2 * m + 1]);
-      bar_arrive(BAR_READY0 + b, 64 + NCONS);
+      bar_arrive(BAR_READY0 + g, 64 + NCONS);
 #pragma unroll 1
-      for (int k = 0; k < NGRP; ++k) cursor_next_active(P, cur);
+      for (int i = 0; i < NGRP; ++i) cursor_next_active(P, cur);
       f += NGRP;
     }
   } else {
@@ -304,15 +318,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma64(const __grid_const
                      : "memory");
       }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    if (c == 0) {  // slot b starts at flat tile b
-      Cursor c0;
-      cursor_start(P, c0);
-      for (int b = 0; b < NBUF; ++b) {
-        slots[b].cur = c0;
-        cursor_next_active(P, c0);
-      }
-      for (int b = 0; b < NBUF; ++b) tma_issue(P, slots[b], b, smem);
-    }
     constexpr int CH = RPT >= 8 ? 8 : 4;
     double acc[RPT];
 #pragma unroll
@@ -329,11 +334,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma64(const __grid_const
       for (int pp = 0; pp < np; ++pp) {
         const uint32_t mk = pp ? __ldg(mrow + (__ffs(pp) - 1) * NCONS) : 0u;
         if (gray(pp) < cnt) {
-          const int b = f % NBUF;
-          const char* bb = reinterpret_cast<const char*>(smem + (size_t)b * BUF_BYTES);
+          const int zg = f % NGRP;
+          const char* bb = reinterpret_cast<const char*>(smem + (size_t)zg * Z_BYTES);
           uint32_t w[2][CH];
           tmem_ld<CH>(taddr, w[0]);  // in flight while waiting for the tile
-          bar_sync(BAR_READY0 + b, 64 + NCONS);
+          bar_sync(BAR_READY0 + zg, 64 + NCONS);
 #pragma unroll
           for (int k = 0; k < RPT; k += CH) {
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -347,19 +352,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma64(const __grid_const
             }
           }
           __syncwarp();
-          if ((c & 31) == 0) {
-            // arrive on EMPTY[b]; a pending count of 1 before this arrival marks the last warp,
-            // which acquires the other warps' arrivals (their reads) and refills the buffer
-            uint64_t st;
-            uint32_t pend;
-            const uint32_t eb = smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b);
-            asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(st) : "r"(eb) : "memory");
-            asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pend) : "l"(st));
-            if (pend == 1) {
-              mbar_wait(eb, (uint32_t)((f / NBUF) & 1));
-              tma_issue(P, slots[b], b, smem);
-            }
-          }
+          if ((c & 31) == 0)  // this warp is done reading z buffer zg
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(smem + CTRL_OFF + CTRL_ZEMPTY + 8 * zg))
+                         : "memory");
           ++f;
         } else {
 #pragma unroll
