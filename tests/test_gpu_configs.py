@@ -117,19 +117,35 @@ def test_config4_full_sampled_columns(lib):
 
 
 def test_config5_full_sampled_columns(lib):
+    # 16 of the 128 columns (15 of A spread over the matrix, and b), element by element, for the
+    # FP32 throughput path and the FP64-accumulation mode; the oracle runs column-parallel on the
+    # host cores (tests/par_oracle.py)
     import torch
-    from oracle import srht as osr
+    from tests import par_oracle
     c = workloads.CONFIGS[5]
     n, d, r = c["n"], c["d"], c["r"]
     M, _ = workloads.dense_device(n, d, seed=workloads.SEED)
-    plan = lib.Plan(n, d, r, workloads.SEED)
-    SM = plan.sketch_columns(M, workspace=plan.workspace(d + 1))
-    torch.cuda.synchronize()
-    SMh = SM.cpu().numpy()
-    for j in [0, 77, d]:  # two A columns and b
-        col = M[:, j].cpu().numpy()
-        ref = osr.sketch(col.astype(np.float64), workloads.SEED, r)
-        assert_tol(SMh[:, j:j + 1], ref, col[:, None])
+    got = {}
+    for accum in ("fp32", "fp64"):
+        plan = lib.Plan(n, d, r, workloads.SEED, accum=accum)
+        got[accum] = plan.sketch_columns(M, workspace=plan.workspace(d + 1)).cpu().numpy().astype(np.float64)
+        assert lib.library().srht_debug_last_kernel() == (3 if accum == "fp32" else 6)
+        del plan
+        torch.cuda.empty_cache()
+    cols = [0, 1, 8, 17, 26, 35, 44, 53, 62, 71, 80, 89, 98, 107, 126, d]
+    bcol = M[:, d].cpu().numpy()
+    specs = [("gen", (j, n)) for j in cols[:-1]] + [("array", bcol)]
+    ref, _ = par_oracle.sketch_columns(specs, workloads.SEED, r)
+    for k, j in enumerate(cols[:-1]):  # the generator pin: the device columns are the host's
+        if k % 5 == 0:
+            assert np.array_equal(M[:, j].cpu().numpy(), workloads.host_uniform_column(workloads.SEED, j, n))
+    colmax = np.array([float(M[:, j].abs().max()) for j in cols])  # max|col| (reading R11)
+    bound = 1e-5 * math.sqrt(n) * np.maximum(colmax, 1e-30)
+    for accum, SM in got.items():
+        err = np.abs(SM[:, cols] - ref)
+        assert np.all(err <= bound[None, :]), (accum, float((err / bound).max()))
+    ulp = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+    assert np.all(np.abs(got["fp64"][:, cols] - ref) <= 2.0 * ulp + 1e-30)
     del M
     torch.cuda.empty_cache()
 
