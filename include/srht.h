@@ -234,6 +234,24 @@ srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G,
                            int64_t stride_x, int32_t* iters, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* ---- NNLS on the Gram form by block principal pivoting (same problem, faster for large d) ----
+ * Same inputs, outputs and iters codes as srht_nnls_gram (Algorithm 1 step 5 via the QP form,
+ * P:311-314 and P:570-590) -- "any standard NNLS solver": the optimum of a
+ * full-column-rank SA is unique, so both solvers return it up to FP64 rounding.  Method
+ * (Portugal, Judice & Vicente 1994; Kim & Park 2011): with F the passive set, x_F solves
+ * Q_FF x_F = q_F, y = Q x - q; the infeasible set V = {i in F: x_i < 0} U {i not in F:
+ * y_i < -tol} (tol = 1e-10 max|q|, the Lawson-Hanson stopping rule) is exchanged whole while
+ * |V| decreases (3 extra tries), else only its largest index; V empty is the KKT point.  Each
+ * step refactors Q_FF (Cholesky); iters[p] = exchange steps, or -1 (cap of 10 d + 10 steps),
+ * -3 (Q_FF not positive definite).  One CTA per problem; d <= 580 (EUNSUPPORTED above).
+ * Workspace: srht_nnls_bpp_workspace_bytes (d x d FP64 per problem), 8-byte aligned.
+ * Device pointers; asynchronous on `stream`.                                  */
+size_t srht_nnls_bpp_workspace_bytes(int64_t d, int64_t batch);
+srht_status srht_nnls_gram_bpp(int64_t d, int64_t batch, const double* G,
+                               int64_t ldg, int64_t stride_g, double* x,
+                               int64_t stride_x, int32_t* iters, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
 /* ---- Algorithm 2, SubspaceSampling ----
  * Row i of Phi (n x d, FP32 column-major, ldphi >= n) is kept with probability
  * q_i = min(1, r p_i) (p: n FP64 probabilities) and scaled by 1/sqrt(q_i): kept

@@ -351,12 +351,15 @@ def gram(SM):
     return G
 
 
-def nnls_gram(G):
-    """Lawson-Hanson NNLS on the Gram form (srht_nnls_gram): x = argmin_{x>=0} x^T Q x - 2 q^T x.
+def nnls_gram(G, method="lh"):
+    """NNLS on the Gram form: x = argmin_{x>=0} x^T Q x - 2 q^T x (Algorithm 1 step 5).
 
     G: float64 CUDA tensor (c, c) or (batch, c, c) from :func:`gram` of [SA | Sb] (c = d + 1).
-    Returns (x, iters): x float64 (d,) or (batch, d); iters int32 (outer iterations, or a
-    negative failure code per problem, see the header).
+    method: "lh" Lawson-Hanson with the oracle's pivot rules (srht_nnls_gram), "bpp" block
+    principal pivoting (srht_nnls_gram_bpp; same optimum, few refactorizations, d <= 580),
+    "auto" = bpp for d > 156 (factor outside shared memory), else lh.
+    Returns (x, iters): x float64 (d,) or (batch, d); iters int32 (iterations, or a negative
+    failure code per problem, see the header).
     """
     torch = _torch()
     lib = _lib.load()
@@ -368,10 +371,15 @@ def nnls_gram(G):
     d = c - 1
     x = torch.empty((batch, d), dtype=torch.float64, device=G.device)
     iters = torch.empty((batch,), dtype=torch.int32, device=G.device)
-    wsb = int(lib.srht_nnls_workspace_bytes(d, batch))
+    if method == "auto":
+        method = "bpp" if d > 156 else "lh"
+    if method not in ("lh", "bpp"):
+        raise ValueError("method must be 'lh', 'bpp' or 'auto'")
+    fn = lib.srht_nnls_gram_bpp if method == "bpp" else lib.srht_nnls_gram
+    wsb = int(lib.srht_nnls_bpp_workspace_bytes(d, batch) if method == "bpp" else lib.srht_nnls_workspace_bytes(d, batch))
     ws = torch.empty((max(wsb, 8) // 8,), dtype=torch.float64, device=G.device)
-    check(lib.srht_nnls_gram(d, batch, Gb.data_ptr(), c, c * c, x.data_ptr(), d, iters.data_ptr(),
-                             ws.data_ptr(), wsb, _stream_ptr(G.device)), "srht_nnls_gram")
+    check(fn(d, batch, Gb.data_ptr(), c, c * c, x.data_ptr(), d, iters.data_ptr(),
+             ws.data_ptr(), wsb, _stream_ptr(G.device)), fn.__name__)
     return (x[0], iters[0]) if single else (x, iters)
 
 

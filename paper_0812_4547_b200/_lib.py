@@ -57,6 +57,8 @@ SIGNATURES = [
     ("srht_subspace_sample_count", ctypes.c_int, [_I64, _I64, _U64, _P, ctypes.POINTER(_I64), _P]),
     ("srht_subspace_sample", ctypes.c_int, [_I64, _I64, _I64, _U64, _P, _P, _I64, _P, _P, _I64, _I64, _P]),
     ("srht_nnls_gram", ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P]),
+    ("srht_nnls_bpp_workspace_bytes", ctypes.c_size_t, [_I64, _I64]),
+    ("srht_nnls_gram_bpp", ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P]),
     ("srht_sketch_rows_partial", ctypes.c_int, [_P, _MP, _I64, _P, _I64, _P, ctypes.c_size_t, _P]),
     ("srht_rows_finish", ctypes.c_int, [_P, _P, _I64, _I64, _P, _I64, _P]),
     ("srht_status_str", ctypes.c_char_p, [ctypes.c_int]),

@@ -749,6 +749,25 @@ srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ld
              : SRHT_ECUDA;
 }
 
+size_t srht_nnls_bpp_workspace_bytes(int64_t d, int64_t batch) {
+  if (d < 1 || batch < 1) return 0;
+  return (size_t)batch * (size_t)d * (size_t)d * sizeof(double);
+}
+
+srht_status srht_nnls_gram_bpp(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
+                               int64_t stride_x, int32_t* iters, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (d < 1 || batch < 1 || !G || !x || ldg < d + 1) return SRHT_EINVAL;
+  if (batch > 1 && (stride_g < ldg * (d + 1) || stride_x < d)) return SRHT_EINVAL;
+  if (!srht::nnls_bpp_ok(d)) return SRHT_EUNSUPPORTED;
+  const size_t need = srht_nnls_bpp_workspace_bytes(d, batch);
+  if (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 7)) return SRHT_EINVAL;
+  return srht::launch_nnls_bpp(d, batch, G, ldg, stride_g, x, stride_x, iters, static_cast<double*>(workspace),
+                               static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
 srht_status srht_subspace_sample_count(int64_t n, int64_t r, uint64_t seed, const double* p, int64_t* kept,
                                        void* stream) {
   if (n < 1 || r < 1 || !p || !kept) return SRHT_EINVAL;

@@ -192,6 +192,10 @@ cudaError_t launch_gram(int64_t r, int64_t c, int64_t batch, const float* SM, in
 
 // Batched Lawson-Hanson NNLS on the Gram form (nnls.cu).
 bool nnls_factor_in_smem(int64_t d);
+// Block principal pivoting NNLS on the Gram form (nnls.cu): d x d FP64 factor per problem in ws.
+bool nnls_bpp_ok(int64_t d);
+cudaError_t launch_nnls_bpp(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
+                            int64_t stride_x, int32_t* iters, double* ws, cudaStream_t stream);
 cudaError_t launch_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
                              int64_t stride_x, int32_t* iters, double* ws, cudaStream_t stream);
 

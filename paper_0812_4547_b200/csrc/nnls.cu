@@ -399,7 +399,309 @@ __global__ void __launch_bounds__(NT) k_nnls_lh_big(int d, const double* __restr
   for (int j = tid; j < d; j += NT) xo[j] = x[j] < 1e-14 ? 0.0 : x[j];
   if (tid == 0 && iters) iters[p] = status ? status : it;
 }
+// ---------------------------------------------------------------------------------------
+// Block principal pivoting (Portugal, Judice & Vicente 1994; Kim & Park 2011) on the Gram form:
+// the same NNLS optimum (unique for a full-column-rank SA, the generic case r >= d+1) reached in
+// a few exchanges of whole index sets instead of one Lawson-Hanson step per entering index.
+// With F the passive set: x_F = Q_FF^{-1} q_F, x = 0 off F, y = Q x - q (y = -w of Lawson-Hanson);
+// infeasible V = {i in F: x_i < 0} U {i not in F: y_i < -tol}, tol = 1e-10 max|q| (the
+// Lawson-Hanson stopping rule); V empty is the KKT point.  Exchange all of V while |V| keeps
+// decreasing (or for up to 3 non-decreasing steps), else only the largest index of V (the backup
+// rule that makes the method finite).  Each step refactors Q_FF (Cholesky, 32-column panels:
+// warp-level diagonal block, row-parallel panel solve, 4 x 4 register tiles for the trailing
+// update from the panel staged in shared memory); the factor lives in the workspace.
+constexpr int PB = 34;  // panel row stride in doubles (16-byte aligned, 16-byte bank shift per row)
+
+struct BppSmem {
+  int m, nv, imax, ninf, pcnt, status, bad;
+};
+
+// Cholesky of the m x m symmetric matrix in F (row-major, stride ld, lower triangle used) in
+// place; returns false if it is not (numerically) positive definite.  panel: (d + 36) x PB doubles
+// (the diagonal block, its reciprocal pivots, then the staged panel rows).  Staged row i goes to
+// physical row (i & 3) * R4 + (i >> 2), so the 4 x 4 tiles' column rows (4 tj + b, consecutive tj
+// across a warp) are consecutive physical rows: conflict-free 16-byte loads.
+__device__ bool bpp_cholesky(double* __restrict__ F, int ld, int m, double* __restrict__ panel, int* bad) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* __restrict__ rinv = panel + (size_t)BK * PB;  // 1 / L[c][c] of the diagonal block (32)
+  double* __restrict__ P = rinv + PB;
+  for (int k0 = 0; k0 < m; k0 += BK) {
+    const int nb = m - k0 < BK ? m - k0 : BK, k1 = k0 + nb;
+    const int mt = m - k1, R4 = (mt + 3) >> 2;
+    if (wid == 0) {  // diagonal block: lane j holds row k0 + j, column sweep with shuffles
+      double Lr[BK];
+#pragma unroll
+      for (int c = 0; c < BK; ++c) Lr[c] = (lane < nb && c <= lane) ? F[(size_t)(k0 + lane) * ld + k0 + c] : 0.0;
+      int fail = 0;
+#pragma unroll
+      for (int c = 0; c < BK; ++c) {
+        if (c < nb) {
+          const double dg = __shfl_sync(0xffffffffu, Lr[c], c);
+          fail |= !(dg > 0.0);
+          const double piv = sqrt(fmax(dg, 1e-300)), ip = 1.0 / piv;
+          Lr[c] = lane == c ? piv : Lr[c] * ip;
+          if (lane == c) rinv[c] = ip;
+#pragma unroll
+          for (int e = c + 1; e < BK; ++e) {
+            const double lec = __shfl_sync(0xffffffffu, Lr[c], e);
+            if (lane >= e && e < nb) Lr[e] -= Lr[c] * lec;
+          }
+        }
+      }
+      if (lane < nb) {
+#pragma unroll
+        for (int c = 0; c < BK; ++c)
+          if (c <= lane) {
+            F[(size_t)(k0 + lane) * ld + k0 + c] = Lr[c];
+            panel[(size_t)lane * PB + c] = Lr[c];  // the diagonal block, for the panel solve
+          }
+      }
+      if (lane == 0 && fail) *bad = 1;
+    }
+    __syncthreads();
+    if (*bad) return false;
+    // panel solve: rows i >= k1, L[i, k0:k1] = F[i, k0:k1] L_kk^{-T} (one row per thread; two
+    // partial sums per entry halve the dependent chain)
+    for (int i = k1 + tid; i < m; i += NT) {
+      double l[BK];
+      double* row = F + (size_t)i * ld + k0;
+#pragma unroll
+      for (int c = 0; c < BK; ++c) l[c] = c < nb ? row[c] : 0.0;
+#pragma unroll
+      for (int c = 0; c < BK; ++c) {
+        if (c < nb) {
+          double a0 = l[c], a1 = 0.0;
+#pragma unroll
+          for (int e = 0; e < c; e += 2) {
+            a0 -= l[e] * panel[(size_t)c * PB + e];
+            if (e + 1 < c) a1 -= l[e + 1] * panel[(size_t)c * PB + e + 1];
+          }
+          l[c] = (a0 + a1) * rinv[c];
+        }
+      }
+      const int ii = i - k1;
+      double* pr = P + (size_t)((ii & 3) * R4 + (ii >> 2)) * PB;
+#pragma unroll
+      for (int c = 0; c < BK; ++c) {
+        if (c < nb) row[c] = l[c];
+        pr[c] = l[c];  // staged (zero-padded to 32 columns)
+      }
+    }
+    // padding rows of the last tile row: zeros
+    for (int ii = mt + tid; ii < 4 * R4; ii += NT) {
+      double* pr = P + (size_t)((ii & 3) * R4 + (ii >> 2)) * PB;
+#pragma unroll
+      for (int c = 0; c < BK; ++c) pr[c] = 0.0;
+    }
+    __syncthreads();
+    // trailing update: F[i][j] -= sum_c P[i][c] P[j][c], k1 <= j <= i < m, 4 x 4 tiles (rows
+    // 4 ti + a, columns 4 tj + b); the 16 F values are loaded before the products
+    const int ntiles = R4 * (R4 + 1) / 2;
+    for (int tix = tid; tix < ntiles; tix += NT) {
+      int ti = (int)((sqrtf(8.f * tix + 1.f) - 1.f) * 0.5f);
+      while ((ti + 1) * (ti + 2) / 2 <= tix) ++ti;
+      while (ti * (ti + 1) / 2 > tix) --ti;
+      const int tj = tix - ti * (ti + 1) / 2;
+      double fv[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = k1 + 4 * ti + a, j = k1 + 4 * tj + b;
+          fv[a][b] = (i < m && j <= i) ? F[(size_t)i * ld + j] : 0.0;
+        }
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 4
+      for (int c = 0; c < BK; c += 2) {
+        double2 pa[4], pb[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          pa[a] = *reinterpret_cast<const double2*>(P + (size_t)(a * R4 + ti) * PB + c);
+          pb[a] = *reinterpret_cast<const double2*>(P + (size_t)(a * R4 + tj) * PB + c);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(pa[a].x, pb[b].x, fma(pa[a].y, pb[b].y, acc[a][b]));
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = k1 + 4 * ti + a;
+        if (i >= m) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int j = k1 + 4 * tj + b;
+          if (j <= i) F[(size_t)i * ld + j] = fv[a][b] - acc[a][b];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(NT) k_nnls_bpp(int d, const double* __restrict__ Gall, int64_t ldg, int64_t stride_g,
+                                                double* __restrict__ xall, int64_t stride_x, int32_t* __restrict__ iters,
+                                                double* __restrict__ ws, int64_t batch) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ BppSmem s;
+  __shared__ NnlsSmem rs;
+  __shared__ double part[BK];
+  const int64_t p = blockIdx.x + (int64_t)blockIdx.y * 65535;
+  if (p >= batch) return;
+  const double* __restrict__ G = Gall + p * stride_g;  // Q[i][j] = G[i + j*ldg], q[i] = G[i + d*ldg]
+  double* x = dsm;          // d: current x
+  double* xs = x + d;       // d: x_F in order positions
+  double* bv = xs + d;      // d
+  double* zt = bv + d;      // d
+  double* panel = zt + d;   // (d + 40) x PB: diagonal block, reciprocal pivots, staged panel (4-row padded)
+  int* order = reinterpret_cast<int*>(panel + (size_t)(d + BK + 8) * PB);
+  unsigned char* inF = reinterpret_cast<unsigned char*>(order + d);
+  unsigned char* vflag = inF + d;  // infeasible in this step
+  double* F = ws + p * (int64_t)d * d;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < d; i += NT) {
+    x[i] = 0.0;
+    inF[i] = 0;
+  }
+  double qm = 0.0;
+  for (int i = tid; i < d; i += NT) qm = fmax(qm, fabs(G[i + d * ldg]));
+  block_argmax(qm, 0, true, rs);
+  const double tol = 1e-10 * fmax(rs.red_v[0], 2.2250738585072014e-308);
+  if (tid == 0) {
+    s.ninf = d + 1;
+    s.pcnt = 3;
+    s.status = 0;
+  }
+  __syncthreads();
+  const int max_iter = 10 * d + 10;
+  int it = 0;
+  while (true) {
+    // order = F ascending (block prefix count over inF)
+    if (tid == 0) {
+      int m = 0;
+      for (int i = 0; i < d; ++i)
+        if (inF[i]) order[m++] = i;
+      s.m = m;
+      s.bad = 0;
+    }
+    __syncthreads();
+    const int m = s.m;
+    // x_F = Q_FF^{-1} q_F (Cholesky in the workspace)
+    {  // Q_FF into the factor storage: warp per row a, lanes over b <= a (Q symmetric: read
+       // column order[a] of G, contiguous in b; write row a of F, contiguous)
+      const int lane = tid & 31, wid = tid >> 5;
+      for (int a = wid; a < m; a += NT / 32) {
+        const double* gc = G + (int64_t)order[a] * ldg;
+        double* fr = F + (size_t)a * d;
+        for (int b = lane; b <= a; b += 32) fr[b] = gc[order[b]];
+      }
+    }
+    __syncthreads();
+    if (m > 0 && !bpp_cholesky(F, d, m, panel, &s.bad)) {
+      if (tid == 0) s.status = -3;
+      __syncthreads();
+      break;
+    }
+    for (int a = tid; a < m; a += NT) bv[a] = G[order[a] + (int64_t)d * ldg];
+    __syncthreads();
+    if (m > 0) {
+      big_fwd(F, d, m, bv, zt, part);
+      big_bwd(F, d, m, zt, xs);
+    }
+    for (int i = tid; i < d; i += NT) x[i] = 0.0;
+    __syncthreads();
+    for (int a = tid; a < m; a += NT) x[order[a]] = xs[a];
+    __syncthreads();
+    // infeasible set: F with x < 0, the rest with y = Q x - q < -tol
+    int nv = 0, imax = -1;
+    for (int i = tid; i < d; i += NT) {
+      bool v;
+      if (inF[i]) {
+        v = x[i] < 0.0;
+      } else {
+        double y = -G[i + d * ldg];
+        for (int a = 0; a < m; ++a) y += G[i + (int64_t)order[a] * ldg] * xs[a];
+        v = y < -tol;
+      }
+      vflag[i] = v;
+      if (v) {
+        ++nv;
+        imax = i;
+      }
+    }
+    // block reductions: count and largest index
+    {
+      int cnt = nv, mx = imax;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      }
+      if (tid == 0) {
+        s.nv = 0;
+        s.imax = -1;
+      }
+      __syncthreads();
+      if ((tid & 31) == 0) {
+        atomicAdd(&s.nv, cnt);
+        atomicMax(&s.imax, mx);
+      }
+      __syncthreads();
+    }
+    const int NV = s.nv;
+    if (NV == 0) break;
+    if (++it > max_iter) {
+      if (tid == 0) s.status = -1;
+      __syncthreads();
+      break;
+    }
+    bool all;
+    if (NV < s.ninf) {
+      all = true;
+    } else {
+      all = s.pcnt > 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (NV < s.ninf) {
+        s.ninf = NV;
+        s.pcnt = 3;
+      } else if (s.pcnt > 0) {
+        s.pcnt -= 1;
+      }
+    }
+    // exchange all of V, or only its largest index (backup rule)
+    const int im = s.imax;
+    for (int i = tid; i < d; i += NT)
+      if (vflag[i] && (all || i == im)) inF[i] ^= 1;
+    __syncthreads();
+  }
+  double* xo = xall + p * stride_x;
+  for (int j = tid; j < d; j += NT) xo[j] = x[j] < 1e-14 ? 0.0 : x[j];
+  if (tid == 0 && iters) iters[p] = s.status ? s.status : it;
+}
 }  // namespace
+
+size_t nnls_bpp_smem_bytes(int64_t d) {
+  return (size_t)(4 * d + (d + BK + 8) * PB) * sizeof(double) + (size_t)d * sizeof(int) + 2 * (size_t)d + 16;
+}
+bool nnls_bpp_ok(int64_t d) { return nnls_bpp_smem_bytes(d) <= 200 * 1024; }
+
+cudaError_t launch_nnls_bpp(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
+                            int64_t stride_x, int32_t* iters, double* ws, cudaStream_t stream) {
+  if (d <= 0 || batch <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)(batch < 65535 ? batch : 65535), (unsigned)((batch + 65534) / 65535));
+  const size_t smem = nnls_bpp_smem_bytes(d);
+  cudaError_t e = cudaFuncSetAttribute(k_nnls_bpp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_nnls_bpp<<<grid, NT, smem, stream>>>((int)d, G, ldg, stride_g, x, stride_x, iters, ws, batch);
+  return cudaGetLastError();
+}
 
 size_t nnls_smem_bytes(int64_t d, bool fac_in_smem) {
   size_t b = (size_t)NNLS_BIG_VEC_DOUBLES(d) * sizeof(double);

@@ -52,9 +52,20 @@ else:
     ws = plan.workspace(c)
     t_s, SM = timed(lambda: plan.sketch_columns(Md, workspace=ws))
 t_g, G = timed(lambda: srht.gram(SM))
-t_n, (x, it) = timed(lambda: srht.nnls_gram(G))
-it = it.cpu().numpy().reshape(-1)
-print(json.dumps({"config": cfg_id, "batch": batch, "n": n, "d": d, "r": r,
-                  "ms": {"sketch": t_s, "gram": t_g, "nnls": t_n, "total": t_s + t_g + t_n},
-                  "nnls_outer_iterations": {"min": int(it.min()), "median": float(np.median(it)), "max": int(it.max())},
-                  "gram_gflops": 2.0 * batch * r * c * c / 2 / (t_g * 1e-3) / 1e9}))
+res = {"config": cfg_id, "batch": batch, "n": n, "d": d, "r": r, "ms": {"sketch": t_s, "gram": t_g},
+       "gram_gflops": 2.0 * batch * r * c * c / 2 / (t_g * 1e-3) / 1e9}
+xs = {}
+for method in ("lh", "bpp"):
+    if method == "bpp" and d > 580:
+        continue
+    t_n, (x, it) = timed(lambda: srht.nnls_gram(G, method=method), reps=3, warm=1)
+    it = it.cpu().numpy().reshape(-1)
+    xs[method] = x
+    res["ms"]["nnls_" + method] = t_n
+    res["iterations_" + method] = {"min": int(it.min()), "median": float(np.median(it)), "max": int(it.max())}
+if len(xs) == 2:
+    a, b = xs["lh"].double(), xs["bpp"].double()
+    res["bpp_vs_lh_max_abs_diff"] = float((a - b).abs().max())
+    res["bpp_vs_lh_same_support"] = bool(torch.equal(a > 0, b > 0))
+res["ms"]["total_bpp" if "nnls_bpp" in res["ms"] else "total_lh"] = t_s + t_g + res["ms"].get("nnls_bpp", res["ms"]["nnls_lh"])
+print(json.dumps(res))

@@ -551,13 +551,19 @@ def test_gram_many_small_problems(lib, batch, c, r):
         assert np.array_equal(G[p], G[p].T)
 
 
-@pytest.mark.parametrize("r,d,zeros", [(64, 8, 4), (512, 50, 20), (2048, 100, 50), (4096, 200, 100), (2048, 300, 150)])
-def test_nnls_gram_matches_lawson_hanson(lib, r, d, zeros):
+@pytest.mark.parametrize("method", ["lh", "bpp"])
+@pytest.mark.parametrize("r,d,zeros", [(64, 8, 4), (512, 50, 20), (2048, 100, 50), (4096, 200, 100), (2048, 300, 150),
+                                       (8192, 512, 256), (600, 33, 0), (300, 40, 40)])
+def test_nnls_gram_matches_lawson_hanson(lib, r, d, zeros, method):
+    # Lawson-Hanson with the oracle's rules and block principal pivoting must both return the
+    # oracle's NNLS optimum (unique: full column rank), same support
     from oracle import nnls
+    if method == "lh" and d > 300:
+        pytest.skip("the d = 512 Lawson-Hanson case runs in the config-4 pipeline test")
     rng = np.random.default_rng(d)
     SA, Sb = _nnls_problem(rng, r, d, zeros)
     G = lib.gram(to_dev(np.column_stack([SA, Sb])))
-    x, it = lib.nnls_gram(G)
+    x, it = lib.nnls_gram(G, method=method)
     x = x.cpu().numpy()
     assert int(it) > 0
     A64, b64 = SA.astype(np.float64), Sb.astype(np.float64)
@@ -604,7 +610,30 @@ def test_randomized_nnls_end_to_end_on_gpu(lib):
     assert abs(Rg - Ro) / Ro <= 1e-6
 
 
-def test_batched_gram_nnls_config2_shape(lib):
+def test_nnls_bpp_ill_conditioned_uniform(lib):
+    # config-4 shape class: nonnegative Uniform[0,1) columns share a large mean direction
+    # (cond(Q) ~ 3 d), d = 512 as in config 4; block principal pivoting against the oracle's LH
+    from oracle import nnls
+    rng = np.random.default_rng(44)
+    r, d = 8192, 512
+    SA = rng.random((r, d), dtype=np.float32)
+    xs = rng.random(d)
+    xs[rng.choice(d, d // 2, replace=False)] = 0.0
+    Sb = (SA.astype(np.float64) @ xs + 0.01 * rng.standard_normal(r)).astype(np.float32)
+    G = lib.gram(to_dev(np.column_stack([SA, Sb])))
+    x, it = lib.nnls_gram(G, method="bpp")
+    x = x.cpu().numpy()
+    assert int(it) > 0
+    A64, b64 = SA.astype(np.float64), Sb.astype(np.float64)
+    xr = nnls.lawson_hanson(A64, b64)[0]
+    f = lambda v: float(np.sum((A64 @ v - b64) ** 2))
+    assert abs(f(x) - f(xr)) <= 1e-10 * f(xr)
+    assert np.array_equal(x > 0, xr > 0)
+    assert nnls.kkt_violation(A64, b64, x) <= 1e-9
+
+
+@pytest.mark.parametrize("method", ["lh", "bpp"])
+def test_batched_gram_nnls_config2_shape(lib, method):
     # config-2 shape class: many independent sparse problems, sketch -> Gram -> NNLS batched
     from oracle import nnls
     w = workloads.config2_host(workloads.SEED, batch=40)
@@ -612,7 +641,7 @@ def test_batched_gram_nnls_config2_shape(lib):
     c = d + 1
     plan = lib.Plan(n, d, r, workloads.SEED, batch=batch)
     SMb = plan.sketch_batched(_csc_dev(w["colptr"], w["rowidx"], w["vals"], (n, batch * c)))
-    x, it = lib.nnls_gram(lib.gram(SMb))
+    x, it = lib.nnls_gram(lib.gram(SMb), method=method)
     x, it, SMh = x.cpu().numpy(), it.cpu().numpy(), SMb.cpu().numpy().astype(np.float64)
     assert np.all(it > 0)
     for p in range(0, batch, 7):
