@@ -212,6 +212,18 @@ srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM,
                       int64_t ldsm, int64_t stride_sm, double* G, int64_t ldg,
                       int64_t stride_g, void* stream);
 
+/* srht_gram with caller-provided scratch (no allocation inside the call).  The products run on
+ * the FP64 tensor cores (DMMA, exact FP32 products, FP64 sums) over 64 x 64 block pairs of the
+ * upper triangle; when a problem has few block pairs the rows are split into K ranges whose
+ * partial blocks are summed in a fixed order (deterministic).  srht_gram_workspace_bytes: the
+ * bytes those partials need (0: none); the workspace must be 256-byte aligned (its contents
+ * on entry do not matter).  srht_gram allocates the same scratch stream-ordered per call.     */
+size_t srht_gram_workspace_bytes(int64_t r, int64_t c, int64_t batch);
+srht_status srht_gram_ex(int64_t r, int64_t c, int64_t batch, const float* SM,
+                         int64_t ldsm, int64_t stride_sm, double* G, int64_t ldg,
+                         int64_t stride_g, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
 /* ---- NNLS on the Gram form (Algorithm 1 step 5, via P:570-590) ----
  * For p < batch: x_p = argmin_{x >= 0} x^T Q x - 2 q^T x, i.e. the NNLS solution
  * of min ||SA x - Sb|| when G_p = [[Q, q], [q^T, .]] = srht_gram([SA | Sb]) is

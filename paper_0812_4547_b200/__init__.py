@@ -338,17 +338,35 @@ def gram(SM):
     if SM.dim() == 3:  # (batch, c, r): block p is column-major r x c with ld = r
         batch, c, r = (int(x) for x in SM.shape)
         SM = SM.contiguous()
-        G = torch.empty((batch, c, c), dtype=torch.float64, device=SM.device)
-        check(lib.srht_gram(r, c, batch, SM.data_ptr(), r, r * c, G.data_ptr(), c, c * c,
-                            _stream_ptr(SM.device)), "srht_gram")
-        return G
-    SM = colmajor(SM)
-    r, c = int(SM.shape[0]), int(SM.shape[1])
-    ld = int(SM.stride(1)) if c > 1 else max(r, 1)
-    G = torch.empty((c, c), dtype=torch.float64, device=SM.device)
-    check(lib.srht_gram(r, c, 1, SM.data_ptr(), ld, ld * c, G.data_ptr(), c, c * c, _stream_ptr(SM.device)),
-          "srht_gram")
-    return G
+        ld, stride = r, r * c
+    else:
+        SM = colmajor(SM)
+        batch, r, c = 1, int(SM.shape[0]), int(SM.shape[1])
+        ld = int(SM.stride(1)) if c > 1 else max(r, 1)
+        stride = ld * c
+    G = torch.empty((batch, c, c), dtype=torch.float64, device=SM.device)
+    wsb = int(lib.srht_gram_workspace_bytes(r, c, batch))
+    ws = _gram_scratch(SM.device, wsb)
+    check(lib.srht_gram_ex(r, c, batch, SM.data_ptr(), ld, stride, G.data_ptr(), c, c * c,
+                           ws.data_ptr() if ws is not None else None, wsb, _stream_ptr(SM.device)), "srht_gram_ex")
+    return G if SM.dim() == 3 else G[0]
+
+
+_GRAM_WS = {}
+
+
+def _gram_scratch(device, nbytes):
+    """256-byte aligned scratch for srht_gram_ex, cached per device.  Calls on different streams
+    of one device must not overlap (torch's current stream orders them)."""
+    if nbytes == 0:
+        return None
+    torch = _torch()
+    key = str(device)
+    buf = _GRAM_WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _GRAM_WS[key] = buf
+    return buf
 
 
 def nnls_gram(G, method="lh"):

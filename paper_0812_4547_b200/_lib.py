@@ -53,6 +53,8 @@ SIGNATURES = [
     ("srht_sketch_columns_host", ctypes.c_int, [_P, _MP, _P, _I64]),
     ("srht_row_shard_rows", ctypes.c_int64, [_P]),
     ("srht_gram", ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P]),
+    ("srht_gram_workspace_bytes", ctypes.c_size_t, [_I64, _I64, _I64]),
+    ("srht_gram_ex", ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P, ctypes.c_size_t, _P]),
     ("srht_nnls_workspace_bytes", ctypes.c_size_t, [_I64, _I64]),
     ("srht_subspace_sample_count", ctypes.c_int, [_I64, _I64, _U64, _P, ctypes.POINTER(_I64), _P]),
     ("srht_subspace_sample", ctypes.c_int, [_I64, _I64, _I64, _U64, _P, _P, _I64, _P, _P, _I64, _I64, _P]),

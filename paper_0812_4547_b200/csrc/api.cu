@@ -726,8 +726,27 @@ srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int6
                       double* G, int64_t ldg, int64_t stride_g, void* stream) {
   if (r < 1 || c < 1 || batch < 1 || !SM || !G || ldsm < r || ldg < c) return SRHT_EINVAL;
   if (batch > 1 && (stride_sm < ldsm * c || stride_g < ldg * c)) return SRHT_EINVAL;
-  return srht::launch_gram(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g, static_cast<cudaStream_t>(stream)) ==
-                 cudaSuccess
+  return srht::launch_gram(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g, nullptr,
+                           static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
+size_t srht_gram_workspace_bytes(int64_t r, int64_t c, int64_t batch) {
+  if (r < 1 || c < 1 || batch < 1) return 0;
+  return srht::gram_workspace_bytes(r, c, batch);
+}
+
+srht_status srht_gram_ex(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
+                         double* G, int64_t ldg, int64_t stride_g, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  if (r < 1 || c < 1 || batch < 1 || !SM || !G || ldsm < r || ldg < c) return SRHT_EINVAL;
+  if (batch > 1 && (stride_sm < ldsm * c || stride_g < ldg * c)) return SRHT_EINVAL;
+  const size_t need = srht::gram_workspace_bytes(r, c, batch);
+  if (need && (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255)))
+    return SRHT_EINVAL;
+  return srht::launch_gram(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g, need ? workspace : nullptr,
+                           static_cast<cudaStream_t>(stream)) == cudaSuccess
              ? SRHT_OK
              : SRHT_ECUDA;
 }

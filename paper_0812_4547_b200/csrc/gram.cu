@@ -220,11 +220,248 @@ __global__ void __launch_bounds__(416) k_gram_tri(int64_t r, int64_t c, int64_t 
       }
     }
 }
+// ---------------------------------------------------------------------------------------
+// FP64 tensor-core Gram (mma.sync m8n8k4 f64 = SASS DMMA; the same 64 FMA/clk/SM as DFMA on the
+// B200, scripts/mb_dmma.cu, but 256 FMA per warp instruction and two 8-byte fragment loads per
+// 256 FMA).  Products of FP32 entries are exact in FP64 and accumulated in FP64, as above.
+// CTA = one 64 x 64 block pair (bi <= bj) of one problem and one K-split; 4 warps, each a
+// 32 x 32 region as 4 x 4 tiles of 8 x 8 (tiles below the diagonal of a diagonal pair and tiles
+// beyond the last column are skipped).  SM rows stream through shared memory as doubles in
+// [column][k] layout (row stride 36 doubles: the fragment loads are conflict-free), 32 rows per
+// step, the next step's rows prefetched into registers.  K-splits write 64 x 64 partials that
+// k_gram_reduce sums in split order, so results are deterministic.
+// Each element is computed once in the upper triangle and mirrored (exactly symmetric).
+constexpr int MB = 64, MKT = 32, MPK = MKT + 4;
+
+template <bool VEC>
+__global__ void __launch_bounds__(128, 4) k_gram_mma(int64_t r, int64_t c, int64_t batch, const float* __restrict__ SM,
+                                                  int64_t ldsm, int64_t stride_sm, double* __restrict__ G, int64_t ldg,
+                                                  int64_t stride_g, int nb, int splits, int64_t kchunk,
+                                                  double* __restrict__ part) {
+  __shared__ __align__(16) double Si[MB][MPK];
+  __shared__ __align__(16) double Sj[MB][MPK];
+  const int npairs = nb * (nb + 1) / 2;
+  const int pair = blockIdx.x / splits, split = blockIdx.x - pair * splits;
+  int rem = pair, bi = 0;
+  while (rem >= nb - bi) {
+    rem -= nb - bi;
+    ++bi;
+  }
+  const int bj = bi + rem;
+  const bool diag = bi == bj;
+  const int64_t p = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  if (p >= batch) return;
+  const float* __restrict__ S = SM + p * stride_sm;
+  const int wi = (int)(c - (int64_t)MB * bi < MB ? c - (int64_t)MB * bi : MB);
+  const int wj = (int)(c - (int64_t)MB * bj < MB ? c - (int64_t)MB * bj : MB);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 1, wc = warp & 1, gid = lane >> 2, tig = lane & 3;
+  const int64_t k_lo = (int64_t)split * kchunk, k_hi = k_lo + kchunk < r ? k_lo + kchunk : r;
+  // tile (ti, tj) of this warp is live iff inside both widths and not below a diagonal block's diagonal
+  bool live[4][4];
+  bool any = false;
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) {
+      const int i8 = 32 * wr + 8 * ti, j8 = 32 * wc + 8 * tj;
+      live[ti][tj] = i8 < wi && j8 < wj && (!diag || i8 <= j8);
+      any |= live[ti][tj];
+    }
+  double acc[4][4][2];
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) acc[ti][tj][0] = acc[ti][tj][1] = 0.0;
+  // staging: element (column cc, rows 4 k4 .. 4 k4 + 3) for idx = tid + 128 u, cc = idx >> 3, k4 = idx & 7
+  float4 pf[2][4];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && diag) break;
+      const int64_t cb = (int64_t)MB * (h ? bj : bi);
+      const int w = h ? wj : wi;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = tid + 128 * u, cc = idx >> 3, k4 = idx & 7;
+        const int64_t k = k0 + 4 * k4;
+        const float* src = S + (cb + cc) * ldsm + k;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (cc < w) {
+          if (VEC && k + 3 < k_hi) {
+            v = __ldg(reinterpret_cast<const float4*>(src));
+          } else {
+            if (k < k_hi) v.x = __ldg(src);
+            if (k + 1 < k_hi) v.y = __ldg(src + 1);
+            if (k + 2 < k_hi) v.z = __ldg(src + 2);
+            if (k + 3 < k_hi) v.w = __ldg(src + 3);
+          }
+        }
+        pf[h][u] = v;
+      }
+    }
+  };
+  fetch(k_lo);
+  for (int64_t k0 = k_lo; k0 < k_hi; k0 += MKT) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && diag) break;
+      double(*D)[MPK] = h ? Sj : Si;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = tid + 128 * u, cc = idx >> 3, k4 = idx & 7;
+        *reinterpret_cast<double2*>(&D[cc][4 * k4]) = make_double2(pf[h][u].x, pf[h][u].y);
+        *reinterpret_cast<double2*>(&D[cc][4 * k4 + 2]) = make_double2(pf[h][u].z, pf[h][u].w);
+      }
+    }
+    __syncthreads();
+    if (k0 + MKT < k_hi) fetch(k0 + MKT);
+    const double(*B)[MPK] = diag ? Si : Sj;
+    if (any) {
+#pragma unroll
+      for (int kk = 0; kk < MKT; kk += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          a[t] = Si[32 * wr + 8 * t + gid][kk + tig];
+          b[t] = B[32 * wc + 8 * t + gid][kk + tig];
+        }
+#pragma unroll
+        for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+          for (int tj = 0; tj < 4; ++tj)
+            if (live[ti][tj])
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(acc[ti][tj][0]), "+d"(acc[ti][tj][1])
+                           : "d"(a[ti]), "d"(b[tj]));
+      }
+    }
+    __syncthreads();
+  }
+  double* __restrict__ Gp = G + p * stride_g;
+  if (splits == 1) {
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) {
+        if (!live[ti][tj]) continue;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int ii = 32 * wr + 8 * ti + gid, jj = 32 * wc + 8 * tj + 2 * tig + e;
+          if (ii < wi && jj < wj && (!diag || ii <= jj)) {
+            const int64_t gi = (int64_t)MB * bi + ii, gj = (int64_t)MB * bj + jj;
+            Gp[gi + gj * ldg] = acc[ti][tj][e];
+            Gp[gj + gi * ldg] = acc[ti][tj][e];
+          }
+        }
+      }
+    return;
+  }
+  // K-split: this split's 64 x 64 partial (k_gram_reduce sums the splits in order)
+  double* __restrict__ mine = part + (((p * npairs + pair) * splits + split) * (MB * MB));
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) {
+      const int ii = 32 * wr + 8 * ti + gid, jj = 32 * wc + 8 * tj + 2 * tig;
+      *reinterpret_cast<double2*>(mine + ii * MB + jj) = make_double2(acc[ti][tj][0], acc[ti][tj][1]);
+    }
+}
+
+// Fixed-order sum of the K-split partials of every block pair (deterministic), upper triangle
+// computed once and mirrored.  Thread = one element of one pair's 64 x 64 block.
+__global__ void k_gram_reduce(int64_t c, int64_t batch, double* __restrict__ G, int64_t ldg, int64_t stride_g, int nb,
+                              int splits, const double* __restrict__ part) {
+  const int npairs = nb * (nb + 1) / 2;
+  const int64_t gidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t slot = gidx / (MB * MB);
+  const int e = (int)(gidx - slot * (MB * MB));
+  if (slot >= (int64_t)npairs * batch) return;
+  const int64_t p = slot / npairs;
+  int rem = (int)(slot - p * npairs), bi = 0;
+  while (rem >= nb - bi) {
+    rem -= nb - bi;
+    ++bi;
+  }
+  const int bj = bi + rem;
+  const int ii = e / MB, jj = e - ii * MB;
+  const int64_t gi = (int64_t)MB * bi + ii, gj = (int64_t)MB * bj + jj;
+  if (gi >= c || gj >= c || gi > gj) return;
+  const double* __restrict__ src = part + slot * splits * (MB * MB) + e;
+  double sum = 0.0;
+  for (int s2 = 0; s2 < splits; ++s2) sum += src[(int64_t)s2 * (MB * MB)];
+  double* __restrict__ Gp = G + p * stride_g;
+  Gp[gi + gj * ldg] = sum;
+  Gp[gj + gi * ldg] = sum;
+}
 }  // namespace
 
+// K-split geometry of the tensor-core Gram: about 4 CTAs per SM (148 SMs), >= 256 rows per split.
+void gram_splits(int64_t r, int64_t c, int64_t batch, int64_t* splits_out, int64_t* kchunk_out, int* npairs_out) {
+  const int nb = (int)((c + MB - 1) / MB);
+  const int npairs = nb * (nb + 1) / 2;
+#ifndef GRAM_CTAS_PER_SM
+#define GRAM_CTAS_PER_SM 8
+#endif
+  int64_t splits = (GRAM_CTAS_PER_SM * 148 + npairs * batch - 1) / (npairs * batch);
+  const int64_t maxs = r / 256 > 1 ? r / 256 : 1;
+  if (splits > maxs) splits = maxs;
+  if (splits < 1) splits = 1;
+  int64_t kchunk = (r + splits - 1) / splits;
+  kchunk = (kchunk + MKT - 1) / MKT * MKT;
+  *splits_out = (r + kchunk - 1) / kchunk;
+  *kchunk_out = kchunk;
+  *npairs_out = npairs;
+}
+
+size_t gram_workspace_bytes(int64_t r, int64_t c, int64_t batch) {
+  int64_t splits, kchunk;
+  int npairs;
+  gram_splits(r, c, batch, &splits, &kchunk, &npairs);
+  if (splits <= 1) return 0;
+  return (size_t)npairs * batch * splits * MB * MB * sizeof(double);
+}
+
+// ws: gram_workspace_bytes bytes (K-split partials); NULL: allocated stream-ordered for this call.
+cudaError_t launch_gram_mma(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
+                            double* G, int64_t ldg, int64_t stride_g, void* ws, cudaStream_t stream) {
+  int64_t splits, kchunk;
+  int npairs;
+  gram_splits(r, c, batch, &splits, &kchunk, &npairs);
+  const int nb = (int)((c + MB - 1) / MB);
+  const bool vec = (ldsm % 4 == 0) && (stride_sm % 4 == 0) && ((reinterpret_cast<uintptr_t>(SM) & 15) == 0);
+  void* own = nullptr;
+  if (splits > 1 && !ws) {
+    const cudaError_t e = cudaMallocAsync(&own, gram_workspace_bytes(r, c, batch), stream);
+    if (e != cudaSuccess) return e;
+    ws = own;
+  }
+  double* part = static_cast<double*>(ws);
+  const dim3 grid((unsigned)(npairs * splits), (unsigned)(batch < 65535 ? batch : 65535), (unsigned)((batch + 65534) / 65535));
+  if (vec)
+    k_gram_mma<true><<<grid, 128, 0, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g, nb, (int)splits,
+                                               kchunk, part);
+  else
+    k_gram_mma<false><<<grid, 128, 0, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g, nb, (int)splits,
+                                                kchunk, part);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && splits > 1) {
+    const int64_t total = (int64_t)npairs * batch * MB * MB;
+    k_gram_reduce<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(c, batch, G, ldg, stride_g, nb, (int)splits,
+                                                                       part);
+    e = cudaGetLastError();
+  }
+  if (own) cudaFreeAsync(own, stream);
+  return e;
+}
+
 cudaError_t launch_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
-                        double* G, int64_t ldg, int64_t stride_g, cudaStream_t stream) {
+                        double* G, int64_t ldg, int64_t stride_g, void* ws, cudaStream_t stream) {
   if (r <= 0 || c <= 0 || batch <= 0) return cudaSuccess;
+#ifndef GRAM_MMA
+#define GRAM_MMA 1
+#endif
+  if (GRAM_MMA) return launch_gram_mma(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g, ws, stream);
   const int nb = (int)((c + GT - 1) / GT);
   const int pairs = nb * (nb + 1) / 2;
   const int64_t zc = (batch + 65534) / 65535;

@@ -188,7 +188,8 @@ extern int g_last_kernel;   // tile kernel of the last srht_sketch* call (bench 
                             // 3 tma, 4 f64, 5 col, 6 tma64
 // Gram matrices of sketches (gram.cu): G_p = SM_p^T SM_p in FP64.
 cudaError_t launch_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
-                        double* G, int64_t ldg, int64_t stride_g, cudaStream_t stream);
+                        double* G, int64_t ldg, int64_t stride_g, void* ws, cudaStream_t stream);
+size_t gram_workspace_bytes(int64_t r, int64_t c, int64_t batch);
 
 // Batched Lawson-Hanson NNLS on the Gram form (nnls.cu).
 bool nnls_factor_in_smem(int64_t d);

@@ -502,9 +502,12 @@ def test_gram_matches_oracle(lib):
     import torch
     from oracle import gram as og
     rng = np.random.default_rng(31)
-    for r, c in [(1000, 37), (8192, 65), (31, 1), (16384, 128)]:
+    for r, c, pad in [(1000, 37, 0), (8192, 65, 0), (31, 1, 0), (16384, 128, 0), (8192, 513, 0), (777, 70, 3),
+                      (4097, 200, 1), (64, 64, 0), (5, 3, 2)]:
         SM = rng.standard_normal((r, c)).astype(np.float32)
-        G = lib.gram(to_dev(SM)).cpu().numpy()
+        dev = torch.zeros((c, r + pad), dtype=torch.float32)
+        dev[:, :r] = torch.from_numpy(SM.T)
+        G = lib.gram(dev.cuda().t()[:r]).cpu().numpy()  # ld = r + pad (unaligned when pad % 4)
         ref = og.gram(SM.astype(np.float64))
         absdot = np.abs(SM.astype(np.float64)).T @ np.abs(SM.astype(np.float64))
         assert np.all(np.abs(G - ref) <= 1e-12 * absdot + 1e-300)
