@@ -584,13 +584,16 @@ def bench_sparse(args, cfg, srht, _lib, world, rank, device):
     kms = statistics.mean(kms_arr[i] for i in range(kcount.value)) if kcount.value else ms
     N = plan.N
     kname = last_kernel(lib)
-    if kname == "k_sketch_col":  # whole-column transform: log2 N stages, no pruned accumulate
-        lb = N.bit_length() - 1
-        adds_per_el = float(lb)
+    # algorithmic adds per padded element with Ailon-Liberty pruning = log2 r + 1
+    # (the kernels' own counts are reported beside it: the whole-column kernel does log2 N, the
+    # tiled kernel log2 B + r / B with B = 2r capped at N)
+    adds_per_el = float((r - 1).bit_length() + 1)
+    if kname == "k_sketch_col":
+        kernel_adds = float(N.bit_length() - 1)
     else:
-        lb = max(10, min(14, (r - 1).bit_length()))
-        adds_per_el = lb + r / float(1 << lb)  # in-tile stages + pruned accumulate
-    adds = adds_per_el * max(N, 1 << lb) * ncols
+        lb = min((r - 1).bit_length() + 1, N.bit_length() - 1, 14)
+        kernel_adds = lb + r / float(1 << lb)
+    adds = adds_per_el * N * ncols
     clk_mhz = clk.summary()["sm_mhz"] or 1965.0
     alu_peak = 148 * 128 * clk_mhz * 1e6 / 1e12  # T adds/s
     value = in_bytes / (ms * 1e-3) / 1e9
@@ -604,6 +607,7 @@ def bench_sparse(args, cfg, srht, _lib, world, rank, device):
         "roofline": {"bound": "alu", "achieved": adds / (kms * 1e-3) / 1e12, "peak": alu_peak, "unit": "Tadd/s",
                      "frac": adds / (kms * 1e-3) / 1e12 / alu_peak, "traffic": None, "kernel": kname,
                      "kernel_ms": kms, "adds_per_padded_element": adds_per_el,
+                     "kernel_adds_per_padded_element": kernel_adds,
                      "hbm_equiv_GBps": (in_bytes + out_bytes) / (kms * 1e-3) / 1e9},
         "clocks": clk.summary(),
         "gpu_launches": args.steps * (2 if plan.workspace_bytes(1) > 0 else 1),

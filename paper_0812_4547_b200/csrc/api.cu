@@ -445,7 +445,10 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
   }
   // Geometry (depends on n and r only).  Tile B ~ r (so ~1 sampled entry per
   // tile row, Ailon-Liberty balance), clamped to [2^10, 2^14]; slabs of ~2^20 rows.
-  int lb = ceil_log2(r);
+  // B = 2r (capped at N): half a gather per element and half the tiles per column of B = r, for
+  // +0.5 adds per element (config 3: 0.105 -> 0.094 ms; B = 4r: 0.115 ms)
+  int lb = ceil_log2(r) + 1;
+  if (lb > ceil_log2(N)) lb = ceil_log2(N);
   // Small columns (N <= 2^12) are transformed as a single tile: fewer
   // sequential sub-blocks per CTA and more threads per column (config 1:
   // 18.7 -> 11.7 us; 2^13 single tiles made config 2 slower, 3.7 -> 6.3 ms).

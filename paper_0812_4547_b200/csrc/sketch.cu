@@ -94,6 +94,9 @@ __device__ __forceinline__ float flip(float x, uint32_t bit) {
 #endif
 template <int RPT>
 __host__ __device__ constexpr bool meta_in_smem() { return V1_META_SMEM && RPT == 32; }
+#ifndef V1_CSC_STAGE
+#define V1_CSC_STAGE 1024  // CSC entries staged in shared memory per CTA (>= threads per CTA)
+#endif
 
 #ifndef V1_THREADS_PER_SM
 #define V1_THREADS_PER_SM 512
@@ -164,20 +167,38 @@ __global__ void __launch_bounds__((1 << LOG_B) / 32, (meta_in_smem<RPT>() ? V1_T
   const int64_t j1 = (j0 + P.J < P.n_sub) ? j0 + P.J : P.n_sub;
   const int64_t n = P.n;
 
-  int64_t cptr = 0, cend = 0;
+  // CSC: the slab's entries [gbase, gend) are staged in shared memory (row, signed value), up to
+  // V1_CSC_STAGE at a time, so the per-tile scatter reads no global memory (config 3: the per-tile
+  // global loads put a DRAM round trip on every tile's critical path)
+  __shared__ int64_t s_end;
+  int* srow = reinterpret_cast<int*>(meta_s + (MS ? RPT * T : 0));
+  float* sval = reinterpret_cast<float*>(srow + V1_CSC_STAGE);
+  int64_t cptr = 0, gbase = 0, gend = 0;
+  int nst = 0;
+  auto stage = [&](int64_t from) {
+    gbase = from;
+    const int64_t left = gend - from;
+    nst = (int)(left < V1_CSC_STAGE ? left : V1_CSC_STAGE);
+    for (int i = tid; i < nst; i += T) {
+      const int row = cs.rowidx[from + i];
+      srow[i] = row;
+      sval[i] = flip(cs.vals[from + i], (__ldg(signs + (row >> 5)) >> (row & 31)) & 1u);
+    }
+  };
   if (cs.fmt == SRHT_CSC) {
-    cend = cs.colptr[lc + 1];
-    if (tid == 0) {
-      int64_t lo = cs.colptr[lc], hi = cend;
-      const int64_t target = j0 * (int64_t)B;
-      while (lo < hi) {  // lower_bound(rowidx, target)
+    if (tid < 2) {  // lower_bound(rowidx, slab start / slab end)
+      int64_t lo = cs.colptr[lc], hi = cs.colptr[lc + 1];
+      const int64_t target = (tid == 0 ? j0 : j1) * (int64_t)B;
+      while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if ((int64_t)cs.rowidx[mid] < target) lo = mid + 1; else hi = mid;
       }
-      s_ptr = lo;
+      if (tid == 0) s_ptr = lo; else s_end = lo;
     }
     __syncthreads();
     cptr = s_ptr;
+    gend = s_end;
+    stage(cptr);
   }
 
   for (int64_t j = j0; j < j1; ++j) {
@@ -203,20 +224,23 @@ __global__ void __launch_bounds__((1 << LOG_B) / 32, (meta_in_smem<RPT>() ? V1_T
         v[2 * h + 1] = make_float2(flip(f.z, (sw >> 2) & 1u), flip(f.w, (sw >> 3) & 1u));
       }
     } else {
-      // CSC: densify the sub-block into the tile (signs applied), then read it.
+      // CSC: densify the sub-block into the tile from the staged entries, then read it.
 #pragma unroll
       for (int i = tid; i < B / 4; i += T) reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncthreads();
-      const int64_t rowend = row0 + B;
+      const int rowend = (int)(row0 + B);
       while (true) {
+        if (cptr + T > gbase + nst && gbase + nst < gend) {  // uniform: restage from cptr
+          stage(cptr);
+          __syncthreads();
+        }
         const int64_t e = cptr + tid;
         bool in = false;
-        if (e < cend) {
-          const int64_t row = cs.rowidx[e];
+        if (e < gbase + nst) {
+          const int row = srow[e - gbase];
           if (row < rowend) {
             in = true;
-            const uint32_t sb = (__ldg(signs + (row >> 5)) >> (row & 31)) & 1u;
-            atomicAdd(&tile[phys((int)(row - row0))], flip(cs.vals[e], sb));
+            atomicAdd(&tile[phys(row - (int)row0)], sval[e - gbase]);  // duplicates are summed
           }
         }
         const int cnt = __syncthreads_count(in);
@@ -315,7 +339,8 @@ __global__ void k_reduce_slabs(const __grid_constant__ SketchParams P, int slab_
 template <int LOG_B, int RPT>
 cudaError_t launch_t(const SketchParams& sp, int64_t items, cudaStream_t stream) {
   constexpr int B = 1 << LOG_B;
-  const size_t smem = (size_t)B * sizeof(float) + (meta_in_smem<RPT>() ? (size_t)RPT * (B / 32) * 4 : 0);
+  const size_t smem = (size_t)B * sizeof(float) + (meta_in_smem<RPT>() ? (size_t)RPT * (B / 32) * 4 : 0) +
+                      (size_t)V1_CSC_STAGE * 8;
   static std::atomic<uint64_t> attr_done{0};
   const cudaError_t e = set_max_dyn_smem_once(k_sketch_tiles<LOG_B, RPT>, (int)smem, attr_done);
   if (e != cudaSuccess) return e;
