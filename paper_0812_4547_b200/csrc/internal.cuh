@@ -141,6 +141,9 @@ extern unsigned long long* g_debug_trace;
 cudaError_t launch_sketch_ws(const srht_plan* P, const WsParams& wp, cudaStream_t stream);
 int ws_phys(int x);  // tile layout of kernel v2 (host side, for the slot layout)
 // Kernel v3 (sketch_tma.cu): dense columns with 16-byte aligned columns (TMA bulk copies).
+#ifndef V3_TMEM_RAW
+#define V3_TMEM_RAW 0  // 1: kernel v3 round 1 reads the raw tile through TMEM (measured slower, DESIGN 11)
+#endif
 #ifndef SRHT_V3_MAX_LOGJ
 #define SRHT_V3_MAX_LOGJ 6
 #endif

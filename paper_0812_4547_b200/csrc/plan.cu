@@ -330,7 +330,10 @@ __global__ void k_permute_signs_v3(const uint32_t* __restrict__ signs32, int64_t
   uint32_t w[4] = {0u, 0u, 0u, 0u};
   for (int h = 0; h < 64; ++h)
     for (int e = 0; e < 2; ++e) {
-      const int64_t row = (T << 14) + e + 2 * p + 256 * h;
+      // register u = e + 2h of producer thread p: rows e + 2p + 256h, or with V3_TMEM_RAW rows
+      // (u & 3) + 4p + 512 (u >> 2)
+      const int u = e + 2 * h;
+      const int64_t row = V3_TMEM_RAW ? (T << 14) + (u & 3) + 4 * p + 512 * (u >> 2) : (T << 14) + e + 2 * p + 256 * h;
       const uint32_t bit = (signs32[row >> 5] >> (row & 31)) & 1u;
       w[h >> 4] |= bit << (((h & 15) << 1) + e);
     }

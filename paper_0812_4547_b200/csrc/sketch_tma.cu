@@ -83,13 +83,21 @@ constexpr bool SPLIT = V3_SPLIT_ISSUE && NQ == 4;
 constexpr int NREF = SPLIT ? V3_REFILL_Q : NQ;
 // control block: FULL mbarriers [0, 8 NQ NBUF), TMEM address [96,100), EMPTY mbarriers
 // [104,128), slot states [128,..)
-constexpr int CTRL_TMEM = 96, CTRL_EMPTY = 104, CTRL_SLOTS = 128, CTRL_BYTES = 384;
+constexpr int CTRL_TMEM = 96, CTRL_EMPTY = 104, CTRL_SLOTS = 128, CTRL_TFULL = 384, CTRL_BYTES = 512;
 static_assert(8 * NQ * NBUF <= CTRL_TMEM, "FULL mbarriers overflow");
 constexpr int SMEM_BYTES = CTRL_OFF + CTRL_BYTES;
 
 enum { BAR_READY0 = 1, BAR_GRP0 = 4, BAR_CONS = 6 };  // named barriers (0 = __syncthreads)
 
+// V3_TMEM_RAW (internal.cuh): round 1 reads the TMA-landed raw tile from tensor memory
+// (tcgen05.cp smem -> TMEM, then tcgen05.ld) instead of with LDS; round 1 then owns row bits
+// {0, 1, 9..13} (thread p = bits 2..8: TMEM lane p holds the 16-byte rows 4p + 512h') and the mid
+// layout's rows/columns follow.
+#if V3_TMEM_RAW
+__host__ __device__ constexpr int mid(int x) { return ((x >> 2) & 127) + ROWW * ((x & 3) | ((x >> 9) << 2)); }
+#else
 __host__ __device__ constexpr int mid(int x) { return ((x >> 1) & 127) + ROWW * ((x & 1) | ((x >> 8) << 1)); }
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -220,7 +228,16 @@ struct SlotState {
 #ifndef V3_L2_HINTS
 #define V3_L2_HINTS 1
 #endif
-static_assert(CTRL_SLOTS + NBUF * sizeof(SlotState) <= CTRL_BYTES, "control block overflows");
+static_assert(CTRL_SLOTS + NBUF * sizeof(SlotState) <= CTRL_TFULL, "control block overflows");
+static_assert(CTRL_TFULL + 8 * NQ * NBUF <= CTRL_BYTES, "control block overflows");
+// TMEM columns: [0, 3 x 128) raw tiles of the three buffers (TMEM_RAW), then the consumers' gather offsets
+constexpr int TRAW_COLS = V3_TMEM_RAW ? NBUF * 128 : 0;
+
+// shared-memory matrix descriptor, no swizzle, K-major canonical layout (8-row core matrices):
+// start address, leading byte offset, stride byte offset 128 (8 rows x 16 B), sm100 version bit
+__device__ __forceinline__ uint64_t desc_nosw(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
+}
 
 __device__ __forceinline__ void tile_src(const V3Params& P, const Cursor& c, int& tile, const float*& src, bool& full) {
   tile = c.s * P.J32 + gray(c.pp);
@@ -308,7 +325,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + CTRL_TMEM);
   SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + CTRL_SLOTS);
   constexpr int MW = RPT;                            // gather byte offsets (TMEM columns) per consumer thread
-  constexpr int TCOLS = (2 * MW) < 32 ? 32 : 2 * MW; // TMEM columns allocated (two consumer warps per lane quarter)
+  // TMEM columns allocated: raw tiles (TMEM_RAW) + gather offsets (two consumer warps per lane quarter)
+  constexpr int TCOLS = V3_TMEM_RAW ? 512 : ((2 * MW) < 32 ? 32 : 2 * MW);
   const int tid = threadIdx.x;
 
   // ---------------- setup (all threads) ----------------
@@ -318,6 +336,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
     for (int b = 0; b < NBUF; ++b)  // EMPTY[b]: one arrival per consumer warp
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b)),
                    "r"(NCONS / 32));
+    if (V3_TMEM_RAW)
+      for (int b = 0; b < NQ * NBUF; ++b)  // TFULL[b][q]: the copies of quarter q into TMEM completed
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(smem + CTRL_OFF + CTRL_TFULL + 8 * b)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid >= 256 && tid < 288) {  // consumer warp 0 allocates TMEM
@@ -383,6 +404,66 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       }
       const uint4 sg = *reinterpret_cast<const uint4*>(smem + SIGN_OFF + 2048 * b + 16 * p);
       float2 v[64];
+#if V3_TMEM_RAW
+      // ---- round 1 from TMEM: rows x = e2 + 4p + 512h' (e2 < 4, h' < 32) = register u = e2 + 4h',
+      // pair m = u >> 1; quarter q = h' in [8q, 8q+8) = m in [16q, 16q+16) ----
+      {
+        const bool tail = row0 + B > n;
+        const uint32_t tq = smem_u32(smem + CTRL_OFF + CTRL_TFULL + 8 * NQ * b);
+        const uint32_t traw = *reinterpret_cast<const uint32_t*>(smem + CTRL_OFF + CTRL_TMEM) + (uint32_t)(128 * b) +
+                              ((uint32_t)(32 * (p >> 5)) << 16);
+        const float* __restrict__ colp = col_ptr(P, cur.col);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q > 0) mbar_wait(fullb + 8 * q, parity);
+          if (p == 0) {
+            if (!tail) {  // quarter q (h' = 8q .. 8q+7) -> TMEM columns 4h' .. 4h'+3 of buffer b
+              const uint32_t t0 = *reinterpret_cast<const uint32_t*>(smem + CTRL_OFF + CTRL_TMEM) + (uint32_t)(128 * b);
+              const uint32_t s0 = smem_u32(smem + (size_t)b * BUF_BYTES);
+#pragma unroll
+              for (int hh = 0; hh < 8; ++hh) {
+                const int hp = 8 * q + hh;
+                asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(t0 + 4 * hp), "l"(desc_nosw(s0 + 2048 * hp)));
+              }
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(tq + 8 * q)
+                           : "memory");
+            } else {
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tq + 8 * q) : "memory");  // keep phases
+            }
+          }
+          uint32_t w[32];
+          if (!tail) {
+            mbar_wait(tq + 8 * q, parity);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                  "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15]),
+                  "=r"(w[16]), "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]), "=r"(w[21]), "=r"(w[22]), "=r"(w[23]),
+                  "=r"(w[24]), "=r"(w[25]), "=r"(w[26]), "=r"(w[27]), "=r"(w[28]), "=r"(w[29]), "=r"(w[30]), "=r"(w[31])
+                : "r"(traw + 32 * q));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          } else {  // ragged tail tile (no TMA data): rows >= n read as zero
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int row = row0 + 4 * p + 512 * (8 * q + (i >> 2)) + (i & 3);
+              w[i] = __float_as_uint(row < n ? colp[row] : 0.f);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[16 * q + i] = make_float2(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1]));
+          const uint32_t wsg = q == 0 ? sg.x : q == 1 ? sg.y : q == 2 ? sg.z : sg.w;
+#pragma unroll
+          for (int h = 16 * q; h < 16 * q + 16; ++h) {
+            const int bt = (h & 15) << 1;
+            v[h].x = flipf(v[h].x, __funnelshift_l(wsg, wsg, 31 - bt) & 0x80000000u);
+            v[h].y = flipf(v[h].y, __funnelshift_l(wsg, wsg, 30 - bt) & 0x80000000u);
+          }
+          fwht_quarter(v, q);  // row bits 0, 1 (pair, m bit 0) and 9..11 (m bits 1..3)
+        }
+      }
+#else
       // ---- round 1: rows x = e + 2p + 256h; quarter q = h in [16q, 16q+16) ----
       if (row0 + B > n) {
         // tail tile (not copied by TMA): the group stages it in the raw layout itself,
@@ -413,6 +494,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
         }
         if (!(DBG & 4)) fwht_quarter(v, q);  // row bit 0 (pair) and bits 8..11 (h bits 0..3)
       }
+#endif
       if (p == 0) { V3_TRACE(g, f, 1) }
 #pragma unroll
       for (int m = 0; m < 64; ++m)
@@ -468,7 +550,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
     const int c = tid - 256;
     const int wc = c >> 5;
     const uint32_t tbase = *tmem_slot;
-    const uint32_t taddr = tbase + ((uint32_t)(32 * (wc & 3)) << 16) + (uint32_t)((wc >> 2) * MW);
+    const uint32_t taddr = tbase + ((uint32_t)(32 * (wc & 3)) << 16) + (uint32_t)(TRAW_COLS + (wc >> 2) * MW);
     // meta -> TMEM (once)
 #pragma unroll
     for (int k = 0; k < MW; k += 4) {
