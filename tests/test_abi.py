@@ -81,3 +81,21 @@ def test_sass_is_sm100a(libpath):
     assert "sm_100a" in out
     sass = subprocess.run([cuobjdump, "-sass", libpath], capture_output=True, text=True).stdout
     assert "FADD2" in sass or "FFMA2" in sass  # packed FP32 butterflies
+
+
+def test_new_entry_points_validate_without_gpu(libpath):
+    # round-2 entry points reject bad arguments before any device work
+    from paper_0812_4547_b200 import _lib
+    lib = _lib.load()
+    E = _lib.SRHT_EINVAL
+    assert lib.srht_rows_finish(None, None, 1, 1, None, 1, None) == E
+    assert lib.srht_gram_ex(0, 1, 1, None, 1, 1, None, 1, 1, None, 0, None) == E
+    assert lib.srht_gram_ex(8, 4, 1, ctypes.c_void_p(256), 4, 32, ctypes.c_void_p(256), 4, 16, None, 0, None) == E
+    assert lib.srht_nnls_gram_bpp(0, 1, None, 1, 1, None, 1, None, None, 0, None) == E
+    assert lib.srht_nnls_gram_bpp(4, 1, ctypes.c_void_p(256), 5, 25, ctypes.c_void_p(256), 4, None, None, 0,
+                                  None) == E  # no workspace
+    assert lib.srht_nnls_gram_bpp(5000, 1, ctypes.c_void_p(256), 5001, 0, ctypes.c_void_p(256), 5000, None,
+                                  ctypes.c_void_p(256), 1 << 30, None) == _lib.SRHT_EUNSUPPORTED
+    assert lib.srht_nnls_bpp_workspace_bytes(512, 2) == 2 * 512 * 512 * 8
+    assert lib.srht_gram_workspace_bytes(8192, 513, 1) > 0       # one problem: K-split partials
+    assert lib.srht_gram_workspace_bytes(1024, 101, 3000) == 0   # many problems: no split

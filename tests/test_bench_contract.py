@@ -34,3 +34,22 @@ def test_reference_arm_json_line():
 def test_reference_arm_only_rank0_prints():
     env = {"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2", "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": "29533"}
     assert _run(env, "--gpus", "2") == []
+
+
+def test_cpu_baseline_workers_bounded():
+    # the all-cores oracle leg: at most one process per host core and per column, at least one
+    sys.path.insert(0, ROOT)
+    import bench
+    for cfg in (1, 4, 5):
+        w, cores = bench.oracle_workers(cfg)
+        assert 1 <= w <= cores == len(os.sched_getaffinity(0))
+        import workloads
+        assert w <= workloads.CONFIGS[cfg]["d"]
+
+
+def test_cpu_baseline_parallel_leg_runs():
+    # two workers on config 1 (tiny): the JSON object carries both legs and the core counts
+    sys.path.insert(0, ROOT)
+    import bench
+    v, t, desc = bench.time_oracle_parallel(1, 2)
+    assert v > 0 and t > 0 and desc.startswith("2 worker processes")
