@@ -632,14 +632,36 @@ def measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device):
         cols = max(1, int(0.6 * avail // (4 * n)))
     host = torch.empty((cols, n), dtype=torch.float32).pin_memory().t()
     host.copy_(Ml[:, :cols])
-    out = torch.empty((cols, r), dtype=torch.float32).pin_memory().t()
-    plan.sketch_columns_host(host, out=out)  # warm-up
+    if world == 1:
+        # one GPU: the host-buffer C-ABI call (chunked H2D / sketch / D2H pipeline inside)
+        out = torch.empty((cols, r), dtype=torch.float32).pin_memory().t()
+
+        def e2e_step():
+            plan.sketch_columns_host(host, out=out)
+        api = "srht_sketch_columns_host (pinned host buffers, chunked H2D/sketch/D2H pipeline)"
+        d2h = 4 * r * cols
+    else:
+        # N GPUs: the public multi-GPU call -- each rank copies its host shard to its device, then
+        # dist.sketch_sharded (sketch + NCCL all-gather), and the full r x c sketch is read back
+        from paper_0812_4547_b200 import dist as sdist
+        full_h = torch.empty((c, r), dtype=torch.float32).pin_memory().t()
+        full_d = torch.empty((c, r), dtype=torch.float32, device=device).t()
+        ws = plan.workspace(cl)
+
+        def e2e_step():
+            Ml[:, :cols].copy_(host, non_blocking=True)
+            sdist.sketch_sharded(plan, Ml, c, out=full_d, workspace=ws)
+            full_h.copy_(full_d, non_blocking=True)
+            torch.cuda.synchronize()
+        api = "host shard -> device (H2D), dist.sketch_sharded (sketch + NCCL all-gather), D2H of the r x c result"
+        d2h = 4 * r * c
+    e2e_step()  # warm-up
     if world > 1:
         dist.barrier()
     ts = []
     for _ in range(max(1, args.e2e_steps)):
         t0 = time.perf_counter()
-        plan.sketch_columns_host(host, out=out)
+        e2e_step()
         ts.append(time.perf_counter() - t0)
     t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=device)
     if world > 1:
@@ -647,8 +669,7 @@ def measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device):
     sec = float(t[0])
     total_cols = cols * world
     e2e = {"value": 4.0 * n * total_cols / sec / 1e9, "unit": UNIT, "h2d_bytes_per_step": 4 * n * cols,
-           "d2h_bytes_per_step": 4 * r * cols, "seconds_per_step": sec,
-           "api": "srht_sketch_columns_host (pinned host buffers, chunked H2D/sketch/D2H pipeline)"}
+           "d2h_bytes_per_step": d2h, "seconds_per_step": sec, "api": api}
     if cols < cl:
         e2e["sample"] = "%d of %d columns per rank (host RAM %.0f GB available)" % (cols, cl, avail / 1e9)
     del host

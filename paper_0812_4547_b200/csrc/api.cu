@@ -6,9 +6,17 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
 
 namespace {
+
+// NVTX range around an entry point (visible in nsys / ncu --nvtx timelines; no cost without a tool)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int ceil_log2(int64_t x) {
   int l = 0;
@@ -395,6 +403,7 @@ const char* srht_status_str(srht_status s) {
 
 srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, int64_t batch, uint32_t flags,
                                 srht_plan** out) {
+  NvtxRange nvtx_("srht_plan_create_ex");
   if (!out) return SRHT_EINVAL;
   *out = nullptr;
   if (n < 1 || d < 0 || r < 1 || batch < 1 || batch > 65535) return SRHT_EINVAL;
@@ -634,6 +643,7 @@ size_t srht_workspace_bytes(const srht_plan* P, int64_t ncols) {
 
 srht_status srht_sketch_columns(const srht_plan* P, const srht_matrix* M, float* SM, int64_t ldsm, void* ws,
                                 size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("srht_sketch_columns");
   if (!P || !valid_matrix(M) || M->rows != P->n || ldsm < P->r) return SRHT_EINVAL;
   if (M->cols > 0 && !SM) return SRHT_EINVAL;
   srht::SketchParams sp = base_params(P);
@@ -646,6 +656,7 @@ srht_status srht_sketch_columns(const srht_plan* P, const srht_matrix* M, float*
 
 srht_status srht_sketch(const srht_plan* P, const srht_matrix* A, const srht_matrix* b, float* SA, int64_t ldsa,
                         float* Sb, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("srht_sketch");
   if (!P || !valid_matrix(A) || A->rows != P->n || ldsa < P->r) return SRHT_EINVAL;
   if (A->cols > 0 && !SA) return SRHT_EINVAL;
   if (b) {
@@ -665,6 +676,7 @@ srht_status srht_sketch(const srht_plan* P, const srht_matrix* A, const srht_mat
 
 srht_status srht_sketch_batched(const srht_plan* P, const srht_matrix* M, float* SM, void* ws, size_t ws_bytes,
                                 void* stream) {
+  NvtxRange nvtx_("srht_sketch_batched");
   if (!P || !valid_matrix(M) || M->rows != P->n || !SM) return SRHT_EINVAL;
   if (M->cols % P->batch != 0 || M->cols == 0) return SRHT_EINVAL;
   srht::SketchParams sp = base_params(P);
@@ -691,6 +703,7 @@ int64_t srht_row_shard_rows(const srht_plan* P) {
 
 srht_status srht_sketch_rows_partial(const srht_plan* P, const srht_matrix* M, int64_t row0, double* part,
                                      int64_t ldp, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("srht_sketch_rows_partial");
   if (!P || !M || !part || P->batch != 1 || ldp < P->r || row0 < 0) return SRHT_EINVAL;
   if (M->rows < 1 || row0 + M->rows > P->n) return SRHT_EINVAL;
   const int64_t g = srht_row_shard_rows(P);
@@ -717,6 +730,7 @@ srht_status srht_sketch_rows_partial(const srht_plan* P, const srht_matrix* M, i
 
 srht_status srht_rows_finish(const srht_plan* P, const double* part, int64_t ldp, int64_t cols, float* SM,
                              int64_t ldsm, void* stream) {
+  NvtxRange nvtx_("srht_rows_finish");
   if (!P || cols < 0 || ldp < P->r || ldsm < P->r) return SRHT_EINVAL;
   if (cols > 0 && (!part || !SM)) return SRHT_EINVAL;
   return srht::launch_rows_finish(part, ldp, P->r, cols, 1.0 / std::sqrt((double)P->r_target), SM, ldsm,
@@ -727,6 +741,7 @@ srht_status srht_rows_finish(const srht_plan* P, const double* part, int64_t ldp
 
 srht_status srht_gram(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
                       double* G, int64_t ldg, int64_t stride_g, void* stream) {
+  NvtxRange nvtx_("srht_gram");
   if (r < 1 || c < 1 || batch < 1 || !SM || !G || ldsm < r || ldg < c) return SRHT_EINVAL;
   if (batch > 1 && (stride_sm < ldsm * c || stride_g < ldg * c)) return SRHT_EINVAL;
   return srht::launch_gram(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g, nullptr,
@@ -743,6 +758,7 @@ size_t srht_gram_workspace_bytes(int64_t r, int64_t c, int64_t batch) {
 srht_status srht_gram_ex(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
                          double* G, int64_t ldg, int64_t stride_g, void* workspace, size_t workspace_bytes,
                          void* stream) {
+  NvtxRange nvtx_("srht_gram_ex");
   if (r < 1 || c < 1 || batch < 1 || !SM || !G || ldsm < r || ldg < c) return SRHT_EINVAL;
   if (batch > 1 && (stride_sm < ldsm * c || stride_g < ldg * c)) return SRHT_EINVAL;
   const size_t need = srht::gram_workspace_bytes(r, c, batch);
@@ -761,6 +777,7 @@ size_t srht_nnls_workspace_bytes(int64_t d, int64_t batch) {
 
 srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
                            int64_t stride_x, int32_t* iters, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("srht_nnls_gram");
   if (d < 1 || batch < 1 || !G || !x || ldg < d + 1 || d > 4096) return SRHT_EINVAL;
   if (batch > 1 && (stride_g < ldg * (d + 1) || stride_x < d)) return SRHT_EINVAL;
   const size_t need = srht_nnls_workspace_bytes(d, batch);
@@ -779,6 +796,7 @@ size_t srht_nnls_bpp_workspace_bytes(int64_t d, int64_t batch) {
 srht_status srht_nnls_gram_bpp(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
                                int64_t stride_x, int32_t* iters, void* workspace, size_t workspace_bytes,
                                void* stream) {
+  NvtxRange nvtx_("srht_nnls_gram_bpp");
   if (d < 1 || batch < 1 || !G || !x || ldg < d + 1) return SRHT_EINVAL;
   if (batch > 1 && (stride_g < ldg * (d + 1) || stride_x < d)) return SRHT_EINVAL;
   if (!srht::nnls_bpp_ok(d)) return SRHT_EUNSUPPORTED;
@@ -801,6 +819,7 @@ srht_status srht_subspace_sample_count(int64_t n, int64_t r, uint64_t seed, cons
 
 srht_status srht_subspace_sample(int64_t n, int64_t d, int64_t r, uint64_t seed, const double* p, const float* Phi,
                                  int64_t ldphi, int32_t* K, float* out, int64_t ldout, int64_t cap, void* stream) {
+  NvtxRange nvtx_("srht_subspace_sample");
   if (n < 1 || d < 0 || r < 1 || !p || !K || cap < 0 || (d > 0 && (!Phi || !out || ldphi < n || ldout < cap)))
     return SRHT_EINVAL;
   return srht::launch_subspace(n, d, r, seed, p, Phi, ldphi, K, out, ldout, cap, nullptr,
@@ -891,6 +910,7 @@ srht_status srht_gen_uniform(uint64_t seed, uint64_t stream0, int64_t rows, int6
 // Host-buffer variant: stream column chunks host -> device, sketch, device -> host,
 // double-buffered over two streams so copies overlap the kernels.
 srht_status srht_sketch_columns_host(const srht_plan* P, const srht_matrix* Mh, float* SMh, int64_t ldsm) {
+  NvtxRange nvtx_("srht_sketch_columns_host");
   if (!P || !valid_matrix(Mh) || Mh->rows != P->n || ldsm < P->r) return SRHT_EINVAL;
   if (Mh->cols == 0) return SRHT_OK;
   if (!SMh) return SRHT_EINVAL;
