@@ -396,6 +396,108 @@ __global__ void k_gram_reduce(int64_t c, int64_t batch, double* __restrict__ G, 
 }
 }  // namespace
 
+// Many small problems (c <= 128, e.g. config 2's 3000 x 101): one CTA per problem stages every
+// column once per 32-row step (a 64 x 64 block pair would stage the columns of both blocks) and its
+// warps share the upper-triangle 8 x 8 tiles row pair by row pair (rows t and nt-1-t: nt+1 tiles per
+// warp, balanced); per k-step a warp loads the fragments of its two tile rows and of the columns it
+// needs once, then issues one DMMA per tile.
+constexpr int SMC = 128, SNT = SMC / 8;  // max columns, max tile rows
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_gram_mma_small(int64_t r, int64_t c, int64_t batch,
+                                                        const float* __restrict__ SM, int64_t ldsm,
+                                                        int64_t stride_sm, double* __restrict__ G, int64_t ldg,
+                                                        int64_t stride_g) {
+  __shared__ __align__(16) double S[SMC][MPK];
+  const int64_t p = blockIdx.x + (int64_t)blockIdx.y * 65535;
+  if (p >= batch) return;
+  const float* __restrict__ Sp = SM + p * stride_sm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gid = lane >> 2, tig = lane & 3;
+  const int nt = (int)((c + 7) >> 3), cp = 8 * nt;
+  const int ra = warp, rb = nt - 1 - warp;  // this warp's tile rows (rb < ra: none; rb == ra: one)
+  const bool has_a = ra < nt && ra <= rb, has_b = has_a && rb != ra;
+  // accumulator slot s (static): s in [ra, nt) -> tile (ra, s); s < ra -> tile (rb, rb + s);
+  // s == SNT -> tile (rb, nt - 1).  Row ra has nt - ra tiles, row rb has ra + 1.
+  double acc[SNT + 1][2];
+#pragma unroll
+  for (int j = 0; j <= SNT; ++j) acc[j][0] = acc[j][1] = 0.0;
+  // staging: (column cc, rows 4 k4 .. 4 k4 + 3) for idx = tid + 256 u < cp * 8
+  constexpr int NU = SMC * 8 / 256;
+  float4 pf[NU];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int idx = tid + 256 * u, cc = idx >> 3, k4 = idx & 7;
+      const int64_t k = k0 + 4 * k4;
+      const float* src = Sp + (int64_t)cc * ldsm + k;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (cc < c) {
+        if (VEC && k + 3 < r) {
+          v = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          if (k < r) v.x = __ldg(src);
+          if (k + 1 < r) v.y = __ldg(src + 1);
+          if (k + 2 < r) v.z = __ldg(src + 2);
+          if (k + 3 < r) v.w = __ldg(src + 3);
+        }
+      }
+      pf[u] = v;
+    }
+  };
+  fetch(0);
+  for (int64_t k0 = 0; k0 < r; k0 += MKT) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int idx = tid + 256 * u, cc = idx >> 3, k4 = idx & 7;
+      if (cc < cp) {
+        *reinterpret_cast<double2*>(&S[cc][4 * k4]) = make_double2(pf[u].x, pf[u].y);
+        *reinterpret_cast<double2*>(&S[cc][4 * k4 + 2]) = make_double2(pf[u].z, pf[u].w);
+      }
+    }
+    __syncthreads();
+    if (k0 + MKT < r) fetch(k0 + MKT);
+    if (has_a) {
+#pragma unroll
+      for (int kk = 0; kk < MKT; kk += 4) {
+        const double fa = S[8 * ra + gid][kk + tig];
+        const double fb = S[8 * rb + gid][kk + tig];
+#pragma unroll
+        for (int sl = 0; sl <= SNT; ++sl) {
+          int j;
+          bool rowb;
+          if (sl == SNT) { j = nt - 1; rowb = true; }
+          else if (sl >= ra) { j = sl; rowb = false; }
+          else { j = rb + sl; rowb = true; }
+          if (j >= nt || (rowb && !has_b)) continue;
+          const double fc = S[8 * j + gid][kk + tig];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[sl][0]), "+d"(acc[sl][1])
+                       : "d"(rowb ? fb : fa), "d"(fc));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!has_a) return;
+  double* __restrict__ Gp = G + p * stride_g;
+#pragma unroll
+  for (int sl = 0; sl <= SNT; ++sl) {
+    int j, ti;
+    if (sl == SNT) { j = nt - 1; ti = rb; }
+    else if (sl >= ra) { j = sl; ti = ra; }
+    else { j = rb + sl; ti = rb; }
+    if (j >= nt || ((sl == SNT || sl < ra) && !has_b)) continue;  // row rb's slots exist only if rb != ra
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t gi = 8 * ti + gid, gj = 8 * j + 2 * tig + e;
+      if (gi < c && gj < c && gi <= gj) {
+        Gp[gi + gj * ldg] = acc[sl][e];
+        Gp[gj + gi * ldg] = acc[sl][e];
+      }
+    }
+  }
+}
+
 // K-split geometry of the tensor-core Gram: about 4 CTAs per SM (148 SMs), >= 256 rows per split.
 void gram_splits(int64_t r, int64_t c, int64_t batch, int64_t* splits_out, int64_t* kchunk_out, int* npairs_out) {
   const int nb = (int)((c + MB - 1) / MB);
@@ -415,6 +517,7 @@ void gram_splits(int64_t r, int64_t c, int64_t batch, int64_t* splits_out, int64
 }
 
 size_t gram_workspace_bytes(int64_t r, int64_t c, int64_t batch) {
+  if (c <= SMC && batch >= 2 * 148) return 0;  // one CTA per problem, no K-split
   int64_t splits, kchunk;
   int npairs;
   gram_splits(r, c, batch, &splits, &kchunk, &npairs);
@@ -425,11 +528,19 @@ size_t gram_workspace_bytes(int64_t r, int64_t c, int64_t batch) {
 // ws: gram_workspace_bytes bytes (K-split partials); NULL: allocated stream-ordered for this call.
 cudaError_t launch_gram_mma(int64_t r, int64_t c, int64_t batch, const float* SM, int64_t ldsm, int64_t stride_sm,
                             double* G, int64_t ldg, int64_t stride_g, void* ws, cudaStream_t stream) {
+  const bool vec = (ldsm % 4 == 0) && (stride_sm % 4 == 0) && ((reinterpret_cast<uintptr_t>(SM) & 15) == 0);
+  if (c <= SMC && batch >= 2 * 148) {  // many small problems: one CTA per problem
+    const dim3 grid((unsigned)(batch < 65535 ? batch : 65535), (unsigned)((batch + 65534) / 65535));
+    if (vec)
+      k_gram_mma_small<true><<<grid, 256, 0, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g);
+    else
+      k_gram_mma_small<false><<<grid, 256, 0, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g);
+    return cudaGetLastError();
+  }
   int64_t splits, kchunk;
   int npairs;
   gram_splits(r, c, batch, &splits, &kchunk, &npairs);
   const int nb = (int)((c + MB - 1) / MB);
-  const bool vec = (ldsm % 4 == 0) && (stride_sm % 4 == 0) && ((reinterpret_cast<uintptr_t>(SM) & 15) == 0);
   void* own = nullptr;
   if (splits > 1 && !ws) {
     const cudaError_t e = cudaMallocAsync(&own, gram_workspace_bytes(r, c, batch), stream);
