@@ -48,6 +48,9 @@ def parse():
                          "(DESIGN.md reading R14), which meets the 1e-6 end-to-end gate on configs 4/5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--sustain-seconds", type=float, default=1.0,
+                    help="after the timed steps, run back to back for about this long and report the "
+                         "steady-state step (the 1000 W board cap engages after ~50 ms); 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", default="columns", choices=["columns", "rows"],
                     help="multi-GPU partition of [A|b]: column ranges + all-gather (default) or "
@@ -458,6 +461,38 @@ def main():
                     else "fallback 6650 GB/s (B200_PROFILING.md)",
                     "kernel_ms": kms_max, "share_of_step": kms_max / ms}
 
+    # ---- sustained: back-to-back steps for ~sustain_seconds, per-step events, second half ----
+    sustained = None
+    if args.sustain_seconds > 0 and not small:
+        k = max(8, int(args.sustain_seconds / (ms * 1e-3)))
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk2:
+            _lib.check(lib.srht_profile_start(k), "srht_profile_start")
+            evs[0].record(stream)
+            for i in range(k):
+                step()
+                evs[i + 1].record(stream)
+            torch.cuda.synchronize()
+            sk_arr = (ctypes.c_float * k)()
+            skc = ctypes.c_int()
+            _lib.check(lib.srht_profile_stop(sk_arr, k, ctypes.byref(skc)), "srht_profile_stop")
+        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(k)]
+        half = per[k // 2:]
+        kh = [sk_arr[i] for i in range(k // 2, skc.value)]
+        st = torch.tensor([statistics.median(half), statistics.median(kh) if kh else 0.0], dtype=torch.float64,
+                          device=device)
+        if world > 1:
+            dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        s_ms, s_kms = float(st[0]), float(st[1])
+        sustained = {"steps": k, "ms_per_step": s_ms, "value": 4.0 * n * c / (s_ms * 1e-3) / 1e9, "unit": UNIT,
+                     "kernel_ms": s_kms, "note": "median of the second half of %d back-to-back steps" % k,
+                     "clocks": clk2.summary()}
+        if args.accum != "fp64" and s_kms > 0:
+            sustained["roofline_frac"] = alg_bytes_launch / (s_kms * 1e-3) / 1e9 / peak
+
     # ---- config 1: steady-state CUDA-graph replay of the step (launch bound) ----
     graph = None
     if small and world == 1 and not rows_mode:
@@ -512,6 +547,8 @@ def main():
         }
         if graph is not None:
             line["graph_replay"] = graph
+        if sustained is not None:
+            line["sustained"] = sustained
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
