@@ -255,8 +255,10 @@ srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G,
  * y_i < -tol} (tol = 1e-10 max|q|, the Lawson-Hanson stopping rule) is exchanged whole while
  * |V| decreases (3 extra tries), else only its largest index; V empty is the KKT point.  Each
  * step refactors Q_FF (Cholesky); iters[p] = exchange steps, or -1 (cap of 10 d + 10 steps),
- * -3 (Q_FF not positive definite).  One CTA per problem; d <= 580 (EUNSUPPORTED above).
- * Workspace: srht_nnls_bpp_workspace_bytes (d x d FP64 per problem), 8-byte aligned.
+ * -3 (Q_FF not positive definite).  One CTA per problem; a single problem with d >= 128 runs on a
+ * thread-block cluster of 16 (else 8) SMs (factorization, panel solves and the dual split over the
+ * cluster).  d <= 580 (EUNSUPPORTED above).  Workspace: srht_nnls_bpp_workspace_bytes (d x d FP64
+ * per problem, plus O(d) vectors for a single problem), 8-byte aligned.
  * Device pointers; asynchronous on `stream`.                                  */
 size_t srht_nnls_bpp_workspace_bytes(int64_t d, int64_t batch);
 srht_status srht_nnls_gram_bpp(int64_t d, int64_t batch, const double* G,

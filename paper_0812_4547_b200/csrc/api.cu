@@ -790,7 +790,12 @@ srht_status srht_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ld
 
 size_t srht_nnls_bpp_workspace_bytes(int64_t d, int64_t batch) {
   if (d < 1 || batch < 1) return 0;
-  return (size_t)batch * (size_t)d * (size_t)d * sizeof(double);
+  const size_t b = (size_t)batch * (size_t)d * (size_t)d * sizeof(double);
+  if (batch == 1) {  // the cluster solver keeps its vectors in the workspace too
+    const size_t c = srht::nnls_bpp_cl_workspace_bytes(d);
+    return c > b ? c : b;
+  }
+  return b;
 }
 
 srht_status srht_nnls_gram_bpp(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,

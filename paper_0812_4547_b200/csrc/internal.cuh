@@ -198,6 +198,7 @@ size_t gram_workspace_bytes(int64_t r, int64_t c, int64_t batch);
 bool nnls_factor_in_smem(int64_t d);
 // Block principal pivoting NNLS on the Gram form (nnls.cu): d x d FP64 factor per problem in ws.
 bool nnls_bpp_ok(int64_t d);
+size_t nnls_bpp_cl_workspace_bytes(int64_t d);  // single large problem on a cluster (batch 1)
 cudaError_t launch_nnls_bpp(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
                             int64_t stride_x, int32_t* iters, double* ws, cudaStream_t stream);
 cudaError_t launch_nnls_gram(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,

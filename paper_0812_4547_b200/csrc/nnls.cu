@@ -685,7 +685,317 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp(int d, const double* __restrict
   for (int j = tid; j < d; j += NT) xo[j] = x[j] < 1e-14 ? 0.0 : x[j];
   if (tid == 0 && iters) iters[p] = s.status ? s.status : it;
 }
+// ---------------------------------------------------------------------------------------
+// The same block principal pivoting for ONE large problem on a thread-block cluster (CS CTAs on
+// CS SMs): the factorization's parallel parts -- gathering Q_FF, the panel solves, the trailing
+// updates -- and the dual y are split over the cluster's CTAs; the diagonal blocks, the
+// triangular solves and the exchange decisions run on rank 0.  The factor and every shared
+// vector live in the workspace (L2); cluster barriers (release / acquire) order the phases.
+// Identical arithmetic per element as k_nnls_bpp except the reduction order of nothing: each F
+// entry and each y_i is still computed by exactly one thread with the same operation order.
+__device__ __forceinline__ void cluster_sync_all() {
+  __threadfence();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
+// workspace layout of the cluster solver (doubles): F (d*d), x, xs, bv, zt (d each), then ints:
+// order (d), inF (d), vflag (d), ctrl (16)
+struct BppClCtrl {
+  int m, nv, imax, ninf, pcnt, status, bad, it;
+};
+
+__device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* __restrict__ panel, int* badg,
+                                int rank, int cs) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int gt = rank * NT + tid, gstride = cs * NT;  // cluster-wide thread index / count
+  double* __restrict__ rinv = panel + (size_t)BK * PB;
+  double* __restrict__ P = rinv + PB;
+  for (int k0 = 0; k0 < m; k0 += BK) {
+    const int nb = m - k0 < BK ? m - k0 : BK, k1 = k0 + nb;
+    const int mt = m - k1, R4 = (mt + 3) >> 2;
+    if (rank == 0 && wid == 0) {  // diagonal block (as in bpp_cholesky), written to F
+      double Lr[BK];
+#pragma unroll
+      for (int c = 0; c < BK; ++c) Lr[c] = (lane < nb && c <= lane) ? F[(size_t)(k0 + lane) * ld + k0 + c] : 0.0;
+      int fail = 0;
+#pragma unroll
+      for (int c = 0; c < BK; ++c) {
+        if (c < nb) {
+          const double dg = __shfl_sync(0xffffffffu, Lr[c], c);
+          fail |= !(dg > 0.0);
+          const double piv = sqrt(fmax(dg, 1e-300)), ip = 1.0 / piv;
+          Lr[c] = lane == c ? piv : Lr[c] * ip;
+#pragma unroll
+          for (int e = c + 1; e < BK; ++e) {
+            const double lec = __shfl_sync(0xffffffffu, Lr[c], e);
+            if (lane >= e && e < nb) Lr[e] -= Lr[c] * lec;
+          }
+        }
+      }
+      if (lane < nb) {
+#pragma unroll
+        for (int c = 0; c < BK; ++c)
+          if (c <= lane) F[(size_t)(k0 + lane) * ld + k0 + c] = Lr[c];
+      }
+      if (lane == 0 && fail) *badg = 1;
+    }
+    cluster_sync_all();
+    if (*(volatile int*)badg) return false;
+    // every CTA: the diagonal block and its reciprocal pivots into shared memory
+    for (int e = tid; e < nb * BK; e += NT) {
+      const int a = e / BK, c = e - a * BK;
+      if (c <= a && a < nb) panel[(size_t)a * PB + c] = F[(size_t)(k0 + a) * ld + k0 + c];
+    }
+    __syncthreads();
+    if (tid < nb) rinv[tid] = 1.0 / panel[(size_t)tid * PB + tid];
+    __syncthreads();
+    // panel solve, rows split over the cluster
+    for (int i = k1 + gt; i < m; i += gstride) {
+      double l[BK];
+      double* row = F + (size_t)i * ld + k0;
+#pragma unroll
+      for (int c = 0; c < BK; ++c) l[c] = c < nb ? row[c] : 0.0;
+#pragma unroll
+      for (int c = 0; c < BK; ++c) {
+        if (c < nb) {
+          double a0 = l[c], a1 = 0.0;
+#pragma unroll
+          for (int e = 0; e < c; e += 2) {
+            a0 -= l[e] * panel[(size_t)c * PB + e];
+            if (e + 1 < c) a1 -= l[e + 1] * panel[(size_t)c * PB + e + 1];
+          }
+          l[c] = (a0 + a1) * rinv[c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < BK; ++c)
+        if (c < nb) row[c] = l[c];
+    }
+    cluster_sync_all();
+    // every CTA stages the whole panel (permuted rows, as bpp_cholesky), then its share of tiles
+    for (int e = tid; e < 4 * R4 * BK; e += NT) {
+      const int ii = e / BK, c = e - ii * BK;
+      double* pr = P + (size_t)((ii & 3) * R4 + (ii >> 2)) * PB;
+      pr[c] = (ii < mt && c < nb) ? F[(size_t)(k1 + ii) * ld + k0 + c] : 0.0;
+    }
+    __syncthreads();
+    const int ntiles = R4 * (R4 + 1) / 2;
+    for (int tix = gt; tix < ntiles; tix += gstride) {
+      int ti = (int)((sqrtf(8.f * tix + 1.f) - 1.f) * 0.5f);
+      while ((ti + 1) * (ti + 2) / 2 <= tix) ++ti;
+      while (ti * (ti + 1) / 2 > tix) --ti;
+      const int tj = tix - ti * (ti + 1) / 2;
+      double fv[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = k1 + 4 * ti + a, j = k1 + 4 * tj + b;
+          fv[a][b] = (i < m && j <= i) ? F[(size_t)i * ld + j] : 0.0;
+        }
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 4
+      for (int c = 0; c < BK; c += 2) {
+        double2 pa[4], pb[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          pa[a] = *reinterpret_cast<const double2*>(P + (size_t)(a * R4 + ti) * PB + c);
+          pb[a] = *reinterpret_cast<const double2*>(P + (size_t)(a * R4 + tj) * PB + c);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(pa[a].x, pb[b].x, fma(pa[a].y, pb[b].y, acc[a][b]));
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = k1 + 4 * ti + a;
+        if (i >= m) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int j = k1 + 4 * tj + b;
+          if (j <= i) F[(size_t)i * ld + j] = fv[a][b] - acc[a][b];
+        }
+      }
+    }
+    cluster_sync_all();
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restrict__ G, int64_t ldg,
+                                                   double* __restrict__ xo, int32_t* __restrict__ iters,
+                                                   double* __restrict__ ws) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ NnlsSmem rs;
+  __shared__ double part[BK];
+  const int rank = (int)cluster_rank(), cs = (int)cluster_size();
+  const int tid = threadIdx.x, gt = rank * NT + tid, gstride = cs * NT;
+  double* F = ws;
+  double* x = F + (size_t)d * d;
+  double* xs = x + d;
+  double* bv = xs + d;
+  double* zt = bv + d;
+  int* order = reinterpret_cast<int*>(zt + d);
+  int* inF = order + d;
+  int* vflag = inF + d;
+  BppClCtrl* ctl = reinterpret_cast<BppClCtrl*>(vflag + d);
+  double* panel = dsm;  // (d + 40) x PB
+  for (int i = gt; i < d; i += gstride) {
+    x[i] = 0.0;
+    inF[i] = 0;
+  }
+  double qm = 0.0;
+  for (int i = tid; i < d; i += NT) qm = fmax(qm, fabs(G[i + (int64_t)d * ldg]));
+  block_argmax(qm, 0, true, rs);
+  const double tol = 1e-10 * fmax(rs.red_v[0], 2.2250738585072014e-308);
+  if (rank == 0 && tid == 0) {
+    ctl->ninf = d + 1;
+    ctl->pcnt = 3;
+    ctl->status = 0;
+    ctl->it = 0;
+  }
+  cluster_sync_all();
+  const int max_iter = 10 * d + 10;
+  while (true) {
+    if (rank == 0 && tid == 0) {
+      int m = 0;
+      for (int i = 0; i < d; ++i)
+        if (inF[i]) order[m++] = i;
+      ctl->m = m;
+      ctl->bad = 0;
+      ctl->nv = 0;
+      ctl->imax = -1;
+    }
+    cluster_sync_all();
+    const int m = *(volatile int*)&ctl->m;
+    {  // Q_FF rows split over the cluster's warps
+      const int lane = tid & 31, gw = rank * (NT / 32) + (tid >> 5);
+      for (int a = gw; a < m; a += cs * (NT / 32)) {
+        const double* gc = G + (int64_t)order[a] * ldg;
+        double* fr = F + (size_t)a * d;
+        for (int b = lane; b <= a; b += 32) fr[b] = gc[order[b]];
+      }
+    }
+    cluster_sync_all();
+    if (m > 0 && !bpp_cholesky_cl(F, d, m, panel, &ctl->bad, rank, cs)) {
+      if (rank == 0 && tid == 0) ctl->status = -3;
+      break;
+    }
+    if (rank == 0) {  // triangular solves on rank 0
+      for (int a = tid; a < m; a += NT) bv[a] = G[order[a] + (int64_t)d * ldg];
+      __syncthreads();
+      if (m > 0) {
+        big_fwd(F, d, m, bv, zt, part);
+        big_bwd(F, d, m, zt, xs);
+      }
+      for (int i = tid; i < d; i += NT) x[i] = 0.0;
+      __syncthreads();
+      for (int a = tid; a < m; a += NT) x[order[a]] = xs[a];
+    }
+    cluster_sync_all();
+    // infeasible set, split over the cluster
+    int nv = 0, imax = -1;
+    for (int i = gt; i < d; i += gstride) {
+      bool v;
+      if (inF[i]) {
+        v = x[i] < 0.0;
+      } else {
+        double y = -G[i + (int64_t)d * ldg];
+        for (int a = 0; a < m; ++a) y += G[i + (int64_t)order[a] * ldg] * xs[a];
+        v = y < -tol;
+      }
+      vflag[i] = v;
+      if (v) {
+        ++nv;
+        imax = i;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      nv += __shfl_xor_sync(0xffffffffu, nv, off);
+      imax = max(imax, __shfl_xor_sync(0xffffffffu, imax, off));
+    }
+    if ((tid & 31) == 0) {
+      if (nv) atomicAdd(&ctl->nv, nv);
+      atomicMax(&ctl->imax, imax);
+    }
+    cluster_sync_all();
+    const int NV = *(volatile int*)&ctl->nv;
+    if (NV == 0) break;
+    const int it = *(volatile int*)&ctl->it + 1;
+    if (it > max_iter) {
+      if (rank == 0 && tid == 0) ctl->status = -1;
+      break;
+    }
+    const int ninf = *(volatile int*)&ctl->ninf, pcnt = *(volatile int*)&ctl->pcnt;
+    const bool all = NV < ninf || pcnt > 0;
+    const int im = *(volatile int*)&ctl->imax;
+    cluster_sync_all();  // everyone has read the decision inputs
+    if (rank == 0 && tid == 0) {
+      ctl->it = it;
+      if (NV < ninf) {
+        ctl->ninf = NV;
+        ctl->pcnt = 3;
+      } else if (pcnt > 0) {
+        ctl->pcnt = pcnt - 1;
+      }
+    }
+    for (int i = gt; i < d; i += gstride)
+      if (vflag[i] && (all || i == im)) inF[i] ^= 1;
+    cluster_sync_all();
+  }
+  cluster_sync_all();
+  if (rank == 0) {
+    for (int j = tid; j < d; j += NT) xo[j] = x[j] < 1e-14 ? 0.0 : x[j];
+    if (tid == 0 && iters) iters[0] = ctl->status ? ctl->status : ctl->it;
+  }
+}
 }  // namespace
+
+size_t nnls_bpp_cl_workspace_bytes(int64_t d) {
+  return ((size_t)d * d + 4 * (size_t)d) * sizeof(double) + 3 * (size_t)d * sizeof(int) + sizeof(BppClCtrl) + 64;
+}
+
+// One problem on a cluster of `cs` CTAs (16: non-portable size, opt-in); returns the launch error
+// (e.g. the cluster cannot be scheduled) so the caller can fall back.
+cudaError_t launch_nnls_bpp_cl(int64_t d, const double* G, int64_t ldg, double* x, int32_t* iters, double* ws,
+                               int cs, cudaStream_t stream) {
+  const size_t smem = (size_t)(d + BK + 8) * PB * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_nnls_bpp_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (cs > 8) {
+    e = cudaFuncSetAttribute(k_nnls_bpp_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cs, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_nnls_bpp_cl, (int)d, G, ldg, x, iters, ws);
+}
 
 size_t nnls_bpp_smem_bytes(int64_t d) {
   return (size_t)(4 * d + (d + BK + 8) * PB) * sizeof(double) + (size_t)d * sizeof(int) + 2 * (size_t)d + 16;
@@ -695,6 +1005,15 @@ bool nnls_bpp_ok(int64_t d) { return nnls_bpp_smem_bytes(d) <= 200 * 1024; }
 cudaError_t launch_nnls_bpp(int64_t d, int64_t batch, const double* G, int64_t ldg, int64_t stride_g, double* x,
                             int64_t stride_x, int32_t* iters, double* ws, cudaStream_t stream) {
   if (d <= 0 || batch <= 0) return cudaSuccess;
+#ifndef BPP_CLUSTER_MIN_D
+#define BPP_CLUSTER_MIN_D 128
+#endif
+  if (batch == 1 && d >= BPP_CLUSTER_MIN_D) {  // one large problem: a cluster of 16 (else 8) SMs
+    for (int cs : {16, 8}) {
+      if (launch_nnls_bpp_cl(d, G, ldg, x, iters, ws, cs, stream) == cudaSuccess) return cudaSuccess;
+      (void)cudaGetLastError();  // not schedulable at this size: try the next
+    }
+  }
   const dim3 grid((unsigned)(batch < 65535 ? batch : 65535), (unsigned)((batch + 65534) / 65535));
   const size_t smem = nnls_bpp_smem_bytes(d);
   cudaError_t e = cudaFuncSetAttribute(k_nnls_bpp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
