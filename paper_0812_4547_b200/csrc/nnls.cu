@@ -22,6 +22,7 @@
 // Q is read from G (L2).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdio.h>
 
 #include "internal.cuh"
 
@@ -438,14 +439,16 @@ __device__ bool bpp_cholesky(double* __restrict__ F, int ld, int m, double* __re
         if (c < nb) {
           const double dg = __shfl_sync(0xffffffffu, Lr[c], c);
           fail |= !(dg > 0.0);
-          const double piv = sqrt(fmax(dg, 1e-300)), ip = 1.0 / piv;
+          // one rsqrt instead of sqrt + divide on the column-to-column dependency chain
+          const double ip = rsqrt(fmax(dg, 1e-300)), piv = dg * ip;
           Lr[c] = lane == c ? piv : Lr[c] * ip;
           if (lane == c) rinv[c] = ip;
+          double lec[BK];
 #pragma unroll
-          for (int e = c + 1; e < BK; ++e) {
-            const double lec = __shfl_sync(0xffffffffu, Lr[c], e);
-            if (lane >= e && e < nb) Lr[e] -= Lr[c] * lec;
-          }
+          for (int e = c + 1; e < BK; ++e) lec[e] = __shfl_sync(0xffffffffu, Lr[c], e);
+#pragma unroll
+          for (int e = c + 1; e < BK; ++e)
+            if (lane >= e && e < nb) Lr[e] -= Lr[c] * lec[e];
         }
       }
       if (lane < nb) {
@@ -693,8 +696,8 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp(int d, const double* __restrict
 // vector live in the workspace (L2); cluster barriers (release / acquire) order the phases.
 // Identical arithmetic per element as k_nnls_bpp except the reduction order of nothing: each F
 // entry and each y_i is still computed by exactly one thread with the same operation order.
+// (release / acquire at cluster scope order the global-memory writes of the cluster's CTAs too)
 __device__ __forceinline__ void cluster_sync_all() {
-  __threadfence();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -714,8 +717,27 @@ struct BppClCtrl {
   int m, nv, imax, ninf, pcnt, status, bad, it;
 };
 
+#ifdef BPP_TRACE
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BPP_T(k) if (rank == 0 && tid == 0) { const unsigned long long t_ = gtime(); tacc[k] += t_ - tlast; tlast = t_; }
+#else
+#define BPP_T(k)
+#endif
+#ifdef BPP_TRACE
+__device__ unsigned long long g_chol_t[4];
+#define BPP_C(k) if (rank == 0 && tid == 0) { const unsigned long long t_ = gtime(); g_chol_t[k] += t_ - tl; tl = t_; }
+#else
+#define BPP_C(k)
+#endif
 __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* __restrict__ panel, int* badg,
                                 int rank, int cs) {
+#ifdef BPP_TRACE
+  unsigned long long tl = gtime();
+#endif
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int gt = rank * NT + tid, gstride = cs * NT;  // cluster-wide thread index / count
   double* __restrict__ rinv = panel + (size_t)BK * PB;
@@ -733,13 +755,14 @@ __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* _
         if (c < nb) {
           const double dg = __shfl_sync(0xffffffffu, Lr[c], c);
           fail |= !(dg > 0.0);
-          const double piv = sqrt(fmax(dg, 1e-300)), ip = 1.0 / piv;
+          const double ip = rsqrt(fmax(dg, 1e-300)), piv = dg * ip;
           Lr[c] = lane == c ? piv : Lr[c] * ip;
+          double lec[BK];
 #pragma unroll
-          for (int e = c + 1; e < BK; ++e) {
-            const double lec = __shfl_sync(0xffffffffu, Lr[c], e);
-            if (lane >= e && e < nb) Lr[e] -= Lr[c] * lec;
-          }
+          for (int e = c + 1; e < BK; ++e) lec[e] = __shfl_sync(0xffffffffu, Lr[c], e);
+#pragma unroll
+          for (int e = c + 1; e < BK; ++e)
+            if (lane >= e && e < nb) Lr[e] -= Lr[c] * lec[e];
         }
       }
       if (lane < nb) {
@@ -750,6 +773,7 @@ __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* _
       if (lane == 0 && fail) *badg = 1;
     }
     cluster_sync_all();
+    BPP_C(0)
     if (*(volatile int*)badg) return false;
     // every CTA: the diagonal block and its reciprocal pivots into shared memory
     for (int e = tid; e < nb * BK; e += NT) {
@@ -757,7 +781,7 @@ __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* _
       if (c <= a && a < nb) panel[(size_t)a * PB + c] = F[(size_t)(k0 + a) * ld + k0 + c];
     }
     __syncthreads();
-    if (tid < nb) rinv[tid] = 1.0 / panel[(size_t)tid * PB + tid];
+    if (tid < nb) rinv[tid] = 1.0 / panel[(size_t)tid * PB + tid];  // (same on every CTA)
     __syncthreads();
     // panel solve, rows split over the cluster
     for (int i = k1 + gt; i < m; i += gstride) {
@@ -782,6 +806,7 @@ __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* _
         if (c < nb) row[c] = l[c];
     }
     cluster_sync_all();
+    BPP_C(1)
     // every CTA stages the whole panel (permuted rows, as bpp_cholesky), then its share of tiles
     for (int e = tid; e < 4 * R4 * BK; e += NT) {
       const int ii = e / BK, c = e - ii * BK;
@@ -789,6 +814,7 @@ __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* _
       pr[c] = (ii < mt && c < nb) ? F[(size_t)(k1 + ii) * ld + k0 + c] : 0.0;
     }
     __syncthreads();
+    BPP_C(2)
     const int ntiles = R4 * (R4 + 1) / 2;
     for (int tix = gt; tix < ntiles; tix += gstride) {
       int ti = (int)((sqrtf(8.f * tix + 1.f) - 1.f) * 0.5f);
@@ -833,8 +859,41 @@ __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* _
       }
     }
     cluster_sync_all();
+    BPP_C(3)
   }
   return true;
+}
+
+// order = the passive indices ascending (block-wide scan of the 0/1 flags in `flag`), m returned
+__device__ int block_compact(const int* __restrict__ flag, int d, int* __restrict__ order, int* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int PER = 4;  // d <= NT * PER
+  int f[PER], cnt = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = tid * PER + k;
+    f[k] = i < d ? flag[i] : 0;
+    cnt += f[k] != 0;
+  }
+  int incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  int base = 0, total = 0;
+  for (int w = 0; w < NT / 32; ++w) {
+    if (w < wid) base += wsum[w];
+    total += wsum[w];
+  }
+  int pos = base + incl - cnt;
+#pragma unroll
+  for (int k = 0; k < PER; ++k)
+    if (f[k]) order[pos++] = tid * PER + k;
+  __syncthreads();
+  return total;
 }
 
 __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restrict__ G, int64_t ldg,
@@ -843,18 +902,21 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restr
   extern __shared__ __align__(16) double dsm[];
   __shared__ NnlsSmem rs;
   __shared__ double part[BK];
+  __shared__ int wsum[NT / 32];
   const int rank = (int)cluster_rank(), cs = (int)cluster_size();
   const int tid = threadIdx.x, gt = rank * NT + tid, gstride = cs * NT;
   double* F = ws;
-  double* x = F + (size_t)d * d;
-  double* xs = x + d;
+  double* x = F + (size_t)d * d;     // global: x (written by rank 0)
+  double* xsg = x + d;                // global: x_F in order positions (written by rank 0)
+  int* inF = reinterpret_cast<int*>(xsg + 3 * d);
+  int* vflag = inF + d;
+  BppClCtrl* ctl = reinterpret_cast<BppClCtrl*>(vflag + 2 * d);
+  // shared memory: panel staging, then per-CTA copies of order and x_F, rank 0's solve vectors
+  double* panel = dsm;  // (d + 40) x PB
+  double* xs = panel + (size_t)(d + BK + 8) * PB;
   double* bv = xs + d;
   double* zt = bv + d;
   int* order = reinterpret_cast<int*>(zt + d);
-  int* inF = order + d;
-  int* vflag = inF + d;
-  BppClCtrl* ctl = reinterpret_cast<BppClCtrl*>(vflag + d);
-  double* panel = dsm;  // (d + 40) x PB
   for (int i = gt; i < d; i += gstride) {
     x[i] = 0.0;
     inF[i] = 0;
@@ -868,21 +930,15 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restr
     ctl->pcnt = 3;
     ctl->status = 0;
     ctl->it = 0;
+    ctl->bad = 0;
   }
   cluster_sync_all();
   const int max_iter = 10 * d + 10;
+#ifdef BPP_TRACE
+  unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0}, tlast = gtime();
+#endif
   while (true) {
-    if (rank == 0 && tid == 0) {
-      int m = 0;
-      for (int i = 0; i < d; ++i)
-        if (inF[i]) order[m++] = i;
-      ctl->m = m;
-      ctl->bad = 0;
-      ctl->nv = 0;
-      ctl->imax = -1;
-    }
-    cluster_sync_all();
-    const int m = *(volatile int*)&ctl->m;
+    const int m = block_compact(inF, d, order, wsum);  // every CTA: its own copy of order
     {  // Q_FF rows split over the cluster's warps
       const int lane = tid & 31, gw = rank * (NT / 32) + (tid >> 5);
       for (int a = gw; a < m; a += cs * (NT / 32)) {
@@ -891,12 +947,18 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restr
         for (int b = lane; b <= a; b += 32) fr[b] = gc[order[b]];
       }
     }
+    if (rank == 0 && tid == 0) {
+      ctl->nv = 0;
+      ctl->imax = -1;
+    }
     cluster_sync_all();
+    BPP_T(0)
     if (m > 0 && !bpp_cholesky_cl(F, d, m, panel, &ctl->bad, rank, cs)) {
       if (rank == 0 && tid == 0) ctl->status = -3;
       break;
     }
-    if (rank == 0) {  // triangular solves on rank 0
+    BPP_T(1)
+    if (rank == 0) {  // triangular solves on rank 0 (vectors in its shared memory)
       for (int a = tid; a < m; a += NT) bv[a] = G[order[a] + (int64_t)d * ldg];
       __syncthreads();
       if (m > 0) {
@@ -905,9 +967,16 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restr
       }
       for (int i = tid; i < d; i += NT) x[i] = 0.0;
       __syncthreads();
-      for (int a = tid; a < m; a += NT) x[order[a]] = xs[a];
+      for (int a = tid; a < m; a += NT) {
+        x[order[a]] = xs[a];
+        xsg[a] = xs[a];
+      }
     }
     cluster_sync_all();
+    BPP_T(2)
+    if (rank != 0)
+      for (int a = tid; a < m; a += NT) xs[a] = xsg[a];
+    __syncthreads();
     // infeasible set, split over the cluster
     int nv = 0, imax = -1;
     for (int i = gt; i < d; i += gstride) {
@@ -935,6 +1004,7 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restr
       atomicMax(&ctl->imax, imax);
     }
     cluster_sync_all();
+    BPP_T(3)
     const int NV = *(volatile int*)&ctl->nv;
     if (NV == 0) break;
     const int it = *(volatile int*)&ctl->it + 1;
@@ -958,8 +1028,15 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restr
     for (int i = gt; i < d; i += gstride)
       if (vflag[i] && (all || i == im)) inF[i] ^= 1;
     cluster_sync_all();
+    BPP_T(4)
   }
   cluster_sync_all();
+#ifdef BPP_TRACE
+  if (rank == 0 && tid == 0)
+    printf("bpp_cl phases us: gather %.1f chol %.1f (diag %.1f panel %.1f stage %.1f trailing %.1f) solves %.1f dual %.1f "
+           "exchange %.1f\n", tacc[0] * 1e-3, tacc[1] * 1e-3, g_chol_t[0] * 1e-3, g_chol_t[1] * 1e-3, g_chol_t[2] * 1e-3,
+           g_chol_t[3] * 1e-3, tacc[2] * 1e-3, tacc[3] * 1e-3, tacc[4] * 1e-3);
+#endif
   if (rank == 0) {
     for (int j = tid; j < d; j += NT) xo[j] = x[j] < 1e-14 ? 0.0 : x[j];
     if (tid == 0 && iters) iters[0] = ctl->status ? ctl->status : ctl->it;
@@ -968,14 +1045,14 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restr
 }  // namespace
 
 size_t nnls_bpp_cl_workspace_bytes(int64_t d) {
-  return ((size_t)d * d + 4 * (size_t)d) * sizeof(double) + 3 * (size_t)d * sizeof(int) + sizeof(BppClCtrl) + 64;
+  return ((size_t)d * d + 4 * (size_t)d) * sizeof(double) + 4 * (size_t)d * sizeof(int) + sizeof(BppClCtrl) + 64;
 }
 
 // One problem on a cluster of `cs` CTAs (16: non-portable size, opt-in); returns the launch error
 // (e.g. the cluster cannot be scheduled) so the caller can fall back.
 cudaError_t launch_nnls_bpp_cl(int64_t d, const double* G, int64_t ldg, double* x, int32_t* iters, double* ws,
                                int cs, cudaStream_t stream) {
-  const size_t smem = (size_t)(d + BK + 8) * PB * sizeof(double);
+  const size_t smem = (size_t)(d + BK + 8) * PB * sizeof(double) + 3 * (size_t)d * sizeof(double) + (size_t)d * sizeof(int);
   cudaError_t e = cudaFuncSetAttribute(k_nnls_bpp_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (cs > 8) {
