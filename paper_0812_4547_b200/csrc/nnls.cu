@@ -733,49 +733,99 @@ __device__ unsigned long long g_chol_t[4];
 #else
 #define BPP_C(k)
 #endif
+// Diagonal block [k0, k0 + nb) of the factor in F, by one warp (lane j holds row k0 + j).
+__device__ __forceinline__ void bpp_diag_warp(double* __restrict__ F, int ld, int k0, int nb, int* badg) {
+  const int lane = threadIdx.x & 31;
+  double Lr[BK];
+#pragma unroll
+  for (int c = 0; c < BK; ++c) Lr[c] = (lane < nb && c <= lane) ? F[(size_t)(k0 + lane) * ld + k0 + c] : 0.0;
+  int fail = 0;
+#pragma unroll
+  for (int c = 0; c < BK; ++c) {
+    if (c < nb) {
+      const double dg = __shfl_sync(0xffffffffu, Lr[c], c);
+      fail |= !(dg > 0.0);
+      const double ip = rsqrt(fmax(dg, 1e-300)), piv = dg * ip;
+      Lr[c] = lane == c ? piv : Lr[c] * ip;
+      double lec[BK];
+#pragma unroll
+      for (int e = c + 1; e < BK; ++e) lec[e] = __shfl_sync(0xffffffffu, Lr[c], e);
+#pragma unroll
+      for (int e = c + 1; e < BK; ++e)
+        if (lane >= e && e < nb) Lr[e] -= Lr[c] * lec[e];
+    }
+  }
+  if (lane < nb) {
+#pragma unroll
+    for (int c = 0; c < BK; ++c)
+      if (c <= lane) F[(size_t)(k0 + lane) * ld + k0 + c] = Lr[c];
+  }
+  if (lane == 0 && fail) *badg = 1;
+}
+
+// 4 x 4 tile (ti, tj) of the trailing update F[i][j] -= sum_c P[i][c] P[j][c] (rows k1 + 4 ti + a,
+// columns k1 + 4 tj + b, j <= i < m) from the staged panel P (permuted rows, see bpp_cholesky)
+__device__ __forceinline__ void bpp_trail_tile(double* __restrict__ F, int ld, int m, int k1, int R4,
+                                               const double* __restrict__ P, int ti, int tj) {
+  double fv[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = k1 + 4 * ti + a, j = k1 + 4 * tj + b;
+      fv[a][b] = (i < m && j <= i) ? F[(size_t)i * ld + j] : 0.0;
+    }
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 4
+  for (int c = 0; c < BK; c += 2) {
+    double2 pa[4], pb[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      pa[a] = *reinterpret_cast<const double2*>(P + (size_t)(a * R4 + ti) * PB + c);
+      pb[a] = *reinterpret_cast<const double2*>(P + (size_t)(a * R4 + tj) * PB + c);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(pa[a].x, pb[b].x, fma(pa[a].y, pb[b].y, acc[a][b]));
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = k1 + 4 * ti + a;
+    if (i >= m) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = k1 + 4 * tj + b;
+      if (j <= i) F[(size_t)i * ld + j] = fv[a][b] - acc[a][b];
+    }
+  }
+}
+
+// Cluster Cholesky with look-ahead: while the other CTAs apply panel k's trailing update to the
+// rest of the matrix, rank 0 updates the next diagonal block first and factors it, so the
+// diagonal chain (a warp of dependent pivots, ~19k cycles per 32 x 32 block) leaves the critical
+// path of all but the first panel.
 __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* __restrict__ panel, int* badg,
                                 int rank, int cs) {
 #ifdef BPP_TRACE
   unsigned long long tl = gtime();
 #endif
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x, wid = tid >> 5;
   const int gt = rank * NT + tid, gstride = cs * NT;  // cluster-wide thread index / count
   double* __restrict__ rinv = panel + (size_t)BK * PB;
   double* __restrict__ P = rinv + PB;
+  if (rank == 0 && wid == 0) bpp_diag_warp(F, ld, 0, m < BK ? m : BK, badg);
+  cluster_sync_all();
+  BPP_C(0)
   for (int k0 = 0; k0 < m; k0 += BK) {
     const int nb = m - k0 < BK ? m - k0 : BK, k1 = k0 + nb;
     const int mt = m - k1, R4 = (mt + 3) >> 2;
-    if (rank == 0 && wid == 0) {  // diagonal block (as in bpp_cholesky), written to F
-      double Lr[BK];
-#pragma unroll
-      for (int c = 0; c < BK; ++c) Lr[c] = (lane < nb && c <= lane) ? F[(size_t)(k0 + lane) * ld + k0 + c] : 0.0;
-      int fail = 0;
-#pragma unroll
-      for (int c = 0; c < BK; ++c) {
-        if (c < nb) {
-          const double dg = __shfl_sync(0xffffffffu, Lr[c], c);
-          fail |= !(dg > 0.0);
-          const double ip = rsqrt(fmax(dg, 1e-300)), piv = dg * ip;
-          Lr[c] = lane == c ? piv : Lr[c] * ip;
-          double lec[BK];
-#pragma unroll
-          for (int e = c + 1; e < BK; ++e) lec[e] = __shfl_sync(0xffffffffu, Lr[c], e);
-#pragma unroll
-          for (int e = c + 1; e < BK; ++e)
-            if (lane >= e && e < nb) Lr[e] -= Lr[c] * lec[e];
-        }
-      }
-      if (lane < nb) {
-#pragma unroll
-        for (int c = 0; c < BK; ++c)
-          if (c <= lane) F[(size_t)(k0 + lane) * ld + k0 + c] = Lr[c];
-      }
-      if (lane == 0 && fail) *badg = 1;
-    }
-    cluster_sync_all();
-    BPP_C(0)
     if (*(volatile int*)badg) return false;
-    // every CTA: the diagonal block and its reciprocal pivots into shared memory
+    // every CTA: the (factored) diagonal block and its reciprocal pivots into shared memory
     for (int e = tid; e < nb * BK; e += NT) {
       const int a = e / BK, c = e - a * BK;
       if (c <= a && a < nb) panel[(size_t)a * PB + c] = F[(size_t)(k0 + a) * ld + k0 + c];
@@ -807,7 +857,8 @@ __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* _
     }
     cluster_sync_all();
     BPP_C(1)
-    // every CTA stages the whole panel (permuted rows, as bpp_cholesky), then its share of tiles
+    if (mt <= 0) break;
+    // every CTA stages the whole panel (permuted rows, as bpp_cholesky)
     for (int e = tid; e < 4 * R4 * BK; e += NT) {
       const int ii = e / BK, c = e - ii * BK;
       double* pr = P + (size_t)((ii & 3) * R4 + (ii >> 2)) * PB;
@@ -815,53 +866,30 @@ __device__ bool bpp_cholesky_cl(double* __restrict__ F, int ld, int m, double* _
     }
     __syncthreads();
     BPP_C(2)
+    // trailing update: tile rows ti < 8 (with tj <= ti) are the next diagonal block: rank 0 applies
+    // them and factors that block; ranks 1.. take every other tile
+    const int ND = 8, nd_tiles = ND * (ND + 1) / 2;
     const int ntiles = R4 * (R4 + 1) / 2;
-    for (int tix = gt; tix < ntiles; tix += gstride) {
-      int ti = (int)((sqrtf(8.f * tix + 1.f) - 1.f) * 0.5f);
-      while ((ti + 1) * (ti + 2) / 2 <= tix) ++ti;
-      while (ti * (ti + 1) / 2 > tix) --ti;
-      const int tj = tix - ti * (ti + 1) / 2;
-      double fv[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int i = k1 + 4 * ti + a, j = k1 + 4 * tj + b;
-          fv[a][b] = (i < m && j <= i) ? F[(size_t)i * ld + j] : 0.0;
-        }
-      double acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-#pragma unroll 4
-      for (int c = 0; c < BK; c += 2) {
-        double2 pa[4], pb[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          pa[a] = *reinterpret_cast<const double2*>(P + (size_t)(a * R4 + ti) * PB + c);
-          pb[a] = *reinterpret_cast<const double2*>(P + (size_t)(a * R4 + tj) * PB + c);
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(pa[a].x, pb[b].x, fma(pa[a].y, pb[b].y, acc[a][b]));
+    if (rank == 0) {
+      for (int tix = tid; tix < nd_tiles && tix < ntiles; tix += NT) {
+        int ti = 0;
+        while ((ti + 1) * (ti + 2) / 2 <= tix) ++ti;
+        bpp_trail_tile(F, ld, m, k1, R4, P, ti, tix - ti * (ti + 1) / 2);
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = k1 + 4 * ti + a;
-        if (i >= m) continue;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int j = k1 + 4 * tj + b;
-          if (j <= i) F[(size_t)i * ld + j] = fv[a][b] - acc[a][b];
-        }
+      __syncthreads();
+      if (wid == 0) bpp_diag_warp(F, ld, k1, mt < BK ? mt : BK, badg);
+    } else {
+      for (int tix = nd_tiles + (rank - 1) * NT + tid; tix < ntiles; tix += (cs - 1) * NT) {
+        int ti = (int)((sqrtf(8.f * tix + 1.f) - 1.f) * 0.5f);
+        while ((ti + 1) * (ti + 2) / 2 <= tix) ++ti;
+        while (ti * (ti + 1) / 2 > tix) --ti;
+        bpp_trail_tile(F, ld, m, k1, R4, P, ti, tix - ti * (ti + 1) / 2);
       }
     }
     cluster_sync_all();
     BPP_C(3)
   }
-  return true;
+  return !*(volatile int*)badg;
 }
 
 // order = the passive indices ascending (block-wide scan of the 0/1 flags in `flag`), m returned
@@ -1006,6 +1034,9 @@ __global__ void __launch_bounds__(NT) k_nnls_bpp_cl(int d, const double* __restr
     cluster_sync_all();
     BPP_T(3)
     const int NV = *(volatile int*)&ctl->nv;
+#ifdef BPP_TRACE
+    if (rank == 0 && tid == 0) printf("bpp_cl step: m %d infeasible %d\n", m, NV);
+#endif
     if (NV == 0) break;
     const int it = *(volatile int*)&ctl->it + 1;
     if (it > max_iter) {
