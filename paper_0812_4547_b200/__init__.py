@@ -369,7 +369,7 @@ def _gram_scratch(device, nbytes):
     return buf
 
 
-def nnls_gram(G, method="lh"):
+def nnls_gram(G, method="auto"):
     """NNLS on the Gram form: x = argmin_{x>=0} x^T Q x - 2 q^T x (Algorithm 1 step 5).
 
     G: float64 CUDA tensor (c, c) or (batch, c, c) from :func:`gram` of [SA | Sb] (c = d + 1).

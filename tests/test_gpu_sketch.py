@@ -589,11 +589,12 @@ def test_nnls_gram_large_d_deterministic(lib):
     rng = np.random.default_rng(7)
     SA, Sb = _nnls_problem(rng, 1024, 240, 120)
     G = lib.gram(to_dev(np.column_stack([SA, Sb])))
-    x0, it0 = lib.nnls_gram(G)
-    for _ in range(3):
-        x1, it1 = lib.nnls_gram(G)
-        assert int(it1) == int(it0)
-        assert torch.equal(x1, x0)
+    for method in ("lh", "bpp"):  # bpp: the single-problem cluster solver (d >= 128)
+        x0, it0 = lib.nnls_gram(G, method=method)
+        for _ in range(3):
+            x1, it1 = lib.nnls_gram(G, method=method)
+            assert int(it1) == int(it0)
+            assert torch.equal(x1, x0)
 
 
 def test_randomized_nnls_end_to_end_on_gpu(lib):
