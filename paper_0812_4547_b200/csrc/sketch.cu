@@ -490,8 +490,6 @@ __global__ void __launch_bounds__(COL_T) k_sketch_col(const __grid_constant__ Sk
 }
 }  // namespace
 
-// Whole-column path: N = 2^13 (the padded tile is 33 KB), one slab per column, outputs
-// written directly (no row shards).  SRHT_V1_COL=0 disables it (experiments).
 // Finish of a row partition: one FP64 scale and one rounding per entry (srht_rows_finish).
 __global__ void k_rows_finish(const double* __restrict__ part, int64_t ldp, int64_t r, int64_t cols, double scale,
                               float* __restrict__ SM, int64_t ldsm) {
@@ -508,6 +506,8 @@ cudaError_t launch_rows_finish(const double* part, int64_t ldp, int64_t r, int64
   return cudaGetLastError();
 }
 
+// Whole-column path: N = 2^13 (the padded tile is 33 KB), one slab per column, outputs
+// written directly (no row shards).
 bool use_col_kernel(const srht_plan* P, const SketchParams& sp) {
   return P->N_eff == COL_N && sp.S_act == 1 && sp.s_lo == 0 && !sp.part_out && P->r <= COL_N;
 }
