@@ -52,6 +52,10 @@ def parse():
                     help="after the timed steps, run back to back for about this long and report the "
                          "steady-state step (the 1000 W board cap engages after ~50 ms); 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1, column shards: p2p = the sketch's reduction stores every rank's columns "
+                         "straight into all ranks' outputs over NVLink (CUDA IPC, fused gather); nccl = one "
+                         "all_gather_into_tensor after the sketch")
     ap.add_argument("--shard", default="columns", choices=["columns", "rows"],
                     help="multi-GPU partition of [A|b]: column ranges + all-gather (default) or "
                          "row ranges + one FP64 all-reduce of the partial sums")
@@ -371,6 +375,15 @@ def main():
     if world > 1:
         from paper_0812_4547_b200 import dist as sdist
         sdist.check_same_plan(plan, device=device)  # untimed: every rank derived the same D and S
+    peers = None
+    gather_mode = "nccl" if (world == 1 or rows_mode) else args.gather
+    if gather_mode == "p2p":
+        try:
+            peers = sdist.PeerOutputs(plan, c)
+        except Exception as exc:  # IPC mapping not possible here: the NCCL all-gather
+            if rank == 0:
+                print("fused gather unavailable (%s); using NCCL all_gather" % exc, file=sys.stderr)
+            gather_mode = "nccl"
         full_out = torch.empty((c, r), dtype=torch.float32, device=device).t()
     else:
         full_out = torch.empty((c, r), dtype=torch.float32, device=device).t()
@@ -386,6 +399,8 @@ def main():
             if world > 1:
                 dist.all_reduce(part_buf.t(), op=dist.ReduceOp.SUM)
             plan.rows_finish(part_buf, out=full_out)  # r^{-1/2} + FP32 rounding in the library
+        elif world > 1 and peers is not None:
+            sdist.sketch_sharded_p2p(plan, Ml, c, peers, workspace=ws)
         elif world > 1:
             sdist.sketch_sharded(plan, Ml, c, out=full_out, workspace=ws)
         else:
@@ -519,7 +534,7 @@ def main():
     # ---- e2e: the same sketch through the host-buffer C-ABI call ----
     e2e = None
     if not args.no_e2e and not rows_mode:
-        e2e = measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device)
+        e2e = measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device, peers)
 
     # ---- cpu_baseline: the oracle on the host cores (rank 0, N = 1 only) ----
     cpu = None
@@ -535,6 +550,8 @@ def main():
                        "accum": args.accum,
                        "columns": c, "input_bytes": total_in,
                        "parallelism": ("rows/%d" if rows_mode else "columns/%d") % world,
+                       "gather": None if world == 1 else ("allreduce (rows)" if rows_mode else
+                                                          ("fused p2p" if peers is not None else "nccl all_gather")),
                        "l2": "flushed (256 MB write) before each step" if small else "inputs larger than L2 (no flush)"},
             "hbm_frac_of_measured": value / peak,
             "hbm_frac_of_8TBs": value / 8000.0,
@@ -657,7 +674,7 @@ def plan_has_reduce(plan):
     return plan.workspace_bytes(1) > 0
 
 
-def measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device):
+def measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device, peers=None):
     """Host-buffer end-to-end: pinned host [A|b] shard -> device -> sketch -> host, every step."""
     import psutil
     import torch
@@ -687,10 +704,14 @@ def measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device):
 
         def e2e_step():
             Ml[:, :cols].copy_(host, non_blocking=True)
-            sdist.sketch_sharded(plan, Ml, c, out=full_d, workspace=ws)
-            full_h.copy_(full_d, non_blocking=True)
+            if peers is not None:
+                res = sdist.sketch_sharded_p2p(plan, Ml, c, peers, workspace=ws)
+            else:
+                res = sdist.sketch_sharded(plan, Ml, c, out=full_d, workspace=ws)
+            full_h.copy_(res, non_blocking=True)
             torch.cuda.synchronize()
-        api = "host shard -> device (H2D), dist.sketch_sharded (sketch + NCCL all-gather), D2H of the r x c result"
+        api = ("host shard -> device (H2D), dist.sketch_sharded%s (sketch + %s), D2H of the r x c result"
+               % (("_p2p", "fused gather over peer memory") if peers is not None else ("", "NCCL all-gather")))
         d2h = 4 * r * c
     e2e_step()  # warm-up
     if world > 1:

@@ -157,6 +157,31 @@ srht_status srht_sketch_columns(const srht_plan* plan, const srht_matrix* M,
                                 float* SM, int64_t ldsm, void* workspace,
                                 size_t workspace_bytes, void* stream);
 
+/* Column shard with the gather fused in (replaces the NCCL all-gather): the sketch of
+ * M's columns (the same values srht_sketch_columns writes) is stored at columns [col0, col0 +
+ * M->cols) of EVERY buffer peers[0..n_peers) (column-major, ld ldp >= r; 1 <= n_peers <= 8).
+ * peers[0] is this rank's own r x c output; peers[1..] are the other ranks' outputs mapped into this
+ * process (CUDA IPC handles or peer access over NVLink).  On the dense TMA path the slab reduction
+ * kernel itself stores every output element into all peers (one kernel: reduce + gather over peer
+ * memory); other paths write peers[0] and one copy kernel stores the block into the others.  The
+ * caller orders the ranks (stream sync + barrier) before reading.  `peers` is a HOST array of device
+ * pointers.  EINVAL on bad arguments (null pointers, n_peers out of range, ldp < r, col0 < 0).
+ * Asynchronous on `stream`.                                                  */
+srht_status srht_sketch_columns_peers(const srht_plan* plan, const srht_matrix* M,
+                                      int64_t col0, float* const* peers,
+                                      int n_peers, int64_t ldp, void* workspace,
+                                      size_t workspace_bytes, void* stream);
+
+/* Buffers for srht_sketch_columns_peers shared across processes (CUDA IPC):
+ * srht_ipc_alloc: device allocation of `bytes` on the current device and its 64-byte IPC handle
+ * (written to `handle`, host memory) for the other ranks; srht_ipc_open: map another process's
+ * allocation from its handle (peer access enabled lazily; NVLink between GPUs); srht_ipc_close:
+ * unmap it; srht_ipc_free: free an srht_ipc_alloc buffer (NULL: no-op).  Synchronous.      */
+srht_status srht_ipc_alloc(size_t bytes, void** dev_ptr, void* handle);
+srht_status srht_ipc_open(const void* handle, void** dev_ptr);
+srht_status srht_ipc_close(void* dev_ptr);
+srht_status srht_ipc_free(void* dev_ptr);
+
 /* Batched mode: M has batch*c columns (problem p owns columns p*c .. p*c+c-1,
  * c = M->cols / batch); output SM is batch blocks of r x c, column-major and
  * contiguous (column g of M lands at SM + g*r).  Problem p uses its own plan.  */

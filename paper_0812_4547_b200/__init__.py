@@ -229,6 +229,17 @@ class Plan:
                                             _stream_ptr(self.device)), "srht_sketch_columns")
         return SM
 
+    def sketch_columns_peers(self, M, col0, peer_ptrs, ld, workspace=None):
+        """Sketch of M's columns stored at columns [col0, col0 + cols) of every buffer in
+        `peer_ptrs` (device addresses, this rank's own output first; ld >= r): the column-shard
+        sketch with the gather fused in (srht_sketch_columns_peers)."""
+        keep = []
+        dM = _describe(M, keep)
+        ws, wsb = self._ws_args(dM.cols, workspace)
+        arr = (ctypes.c_void_p * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
+        check(self._lib.srht_sketch_columns_peers(self._h, ctypes.byref(dM), int(col0), arr, len(peer_ptrs), int(ld),
+                                                  ws, wsb, _stream_ptr(self.device)), "srht_sketch_columns_peers")
+
     def row_shard_rows(self):
         """Row granularity of row shards (srht_row_shard_rows)."""
         return int(self._lib.srht_row_shard_rows(self._h))

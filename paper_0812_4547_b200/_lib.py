@@ -49,6 +49,8 @@ SIGNATURES = [
     ("srht_workspace_bytes", ctypes.c_size_t, [_P, _I64]),
     ("srht_sketch", ctypes.c_int, [_P, _MP, _MP, _P, _I64, _P, _P, ctypes.c_size_t, _P]),
     ("srht_sketch_columns", ctypes.c_int, [_P, _MP, _P, _I64, _P, ctypes.c_size_t, _P]),
+    ("srht_sketch_columns_peers", ctypes.c_int, [_P, _MP, _I64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, _I64,
+                                                 _P, ctypes.c_size_t, _P]),
     ("srht_sketch_batched", ctypes.c_int, [_P, _MP, _P, _P, ctypes.c_size_t, _P]),
     ("srht_sketch_columns_host", ctypes.c_int, [_P, _MP, _P, _I64]),
     ("srht_row_shard_rows", ctypes.c_int64, [_P]),
@@ -63,6 +65,10 @@ SIGNATURES = [
     ("srht_nnls_gram_bpp", ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P]),
     ("srht_sketch_rows_partial", ctypes.c_int, [_P, _MP, _I64, _P, _I64, _P, ctypes.c_size_t, _P]),
     ("srht_rows_finish", ctypes.c_int, [_P, _P, _I64, _I64, _P, _I64, _P]),
+    ("srht_ipc_alloc", ctypes.c_int, [ctypes.c_size_t, _PP, _P]),
+    ("srht_ipc_open", ctypes.c_int, [_P, _PP]),
+    ("srht_ipc_close", ctypes.c_int, [_P]),
+    ("srht_ipc_free", ctypes.c_int, [_P]),
     ("srht_status_str", ctypes.c_char_p, [ctypes.c_int]),
     ("srht_gen_uniform", ctypes.c_int, [_U64, _U64, _I64, _I64, _P, _I64, _P]),
     ("srht_profile_start", ctypes.c_int, [ctypes.c_int]),

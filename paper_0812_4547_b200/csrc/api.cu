@@ -654,6 +654,66 @@ srht_status srht_sketch_columns(const srht_plan* P, const srht_matrix* M, float*
   return run(P, sp, ws, ws_bytes, stream);
 }
 
+srht_status srht_ipc_alloc(size_t bytes, void** dev_ptr, void* handle) {
+  if (!dev_ptr || !handle || bytes == 0) return SRHT_EINVAL;
+  *dev_ptr = nullptr;
+  if (cudaMalloc(dev_ptr, bytes) != cudaSuccess) return SRHT_ENOMEM;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, *dev_ptr) != cudaSuccess) {
+    cudaFree(*dev_ptr);
+    *dev_ptr = nullptr;
+    return SRHT_ECUDA;
+  }
+  std::memcpy(handle, &h, sizeof(h));
+  return SRHT_OK;
+}
+
+srht_status srht_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return SRHT_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+}
+
+srht_status srht_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return SRHT_EINVAL;
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+}
+
+srht_status srht_ipc_free(void* dev_ptr) {
+  if (!dev_ptr) return SRHT_OK;
+  return cudaFree(dev_ptr) == cudaSuccess ? SRHT_OK : SRHT_ECUDA;
+}
+
+srht_status srht_sketch_columns_peers(const srht_plan* P, const srht_matrix* M, int64_t col0, float* const* peers,
+                                      int n_peers, int64_t ldp, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("srht_sketch_columns_peers");
+  if (!P || !valid_matrix(M) || M->rows != P->n || ldp < P->r || col0 < 0 || !peers) return SRHT_EINVAL;
+  if (n_peers < 1 || n_peers > SRHT_MAX_PEERS) return SRHT_EINVAL;
+  for (int k = 0; k < n_peers; ++k)
+    if (!peers[k]) return SRHT_EINVAL;
+  if (M->cols == 0) return SRHT_OK;
+  srht::SketchParams sp = base_params(P);
+  float* local = peers[0] + col0 * ldp;
+  sp.src[0] = make_src(M, local, ldp);
+  sp.ncols0 = M->cols;
+  sp.total_cols = M->cols;
+  sp.cols_per_problem = INT64_MAX;
+  sp.n_peers = n_peers;
+  for (int k = 0; k < n_peers; ++k) sp.peers[k] = peers[k];
+  sp.peer_col0 = col0;
+  sp.peer_ld = ldp;
+  srht::g_last_kernel = 0;
+  const srht_status st = run(P, sp, ws, ws_bytes, stream);
+  if (st != SRHT_OK) return st;
+  if (srht::g_last_kernel == 3) return SRHT_OK;  // kernel v3's reduction stored into every peer
+  // other paths: one copy kernel from the primary output into the peers
+  return srht::launch_peer_copy(local, ldp, P->r, M->cols, peers, n_peers, col0, ldp,
+                                static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SRHT_OK
+             : SRHT_ECUDA;
+}
+
 srht_status srht_sketch(const srht_plan* P, const srht_matrix* A, const srht_matrix* b, float* SA, int64_t ldsa,
                         float* Sb, void* ws, size_t ws_bytes, void* stream) {
   NvtxRange nvtx_("srht_sketch");

@@ -91,6 +91,7 @@ struct ColSrc {
   int64_t ldo;
 };
 
+#define SRHT_MAX_PEERS 8
 struct SketchParams {
   ColSrc src[2];
   int64_t ncols0;             // columns of src[0]; src[1] follows
@@ -113,6 +114,11 @@ struct SketchParams {
   double* partials64;         // FP64 mode: [S_act][total_cols][r] when S_act > 1 or part_out
   double* part_out;           // row-shard mode: unscaled FP64 partial sums, column j at part_out + j*ldp
   int64_t ldp;
+  // fused gather (srht_sketch_columns_peers): kernel v3's reduction also stores output column j at
+  // column peer_col0 + j of every peer buffer (ld peer_ld); peers[0] is the primary output
+  float* peers[SRHT_MAX_PEERS];
+  int n_peers;
+  int64_t peer_col0, peer_ld;
 };
 // FP64-accumulation parity mode (sketch_f64.cu), v1 slab geometry.
 cudaError_t launch_sketch_f64(const srht_plan* P, const SketchParams& sp, cudaStream_t stream);
@@ -185,6 +191,9 @@ cudaError_t build_v64_signs(const uint64_t* signs, int64_t n_tiles, uint2* out, 
 // Slab reduction of kernel v3's slot-order partials (sp.partials, S_act, s_lo, outputs).
 cudaError_t launch_reduce_v3(const SketchParams& sp, const uint32_t* ttab, int rpt, int slab_shift,
                              cudaStream_t stream);
+// Copy r x cols FP32 (column-major, ld src_ld) to every peer buffer at column col0 (ld peer_ld).
+cudaError_t launch_peer_copy(const float* src, int64_t src_ld, int64_t r, int64_t cols, float* const* peers,
+                             int n_peers, int64_t col0, int64_t peer_ld, cudaStream_t stream);
 int v3_mid(int x);  // kernel-v3 z layout (host side, for the slot layout)
 extern int g_kernel_force;  // 0 auto, 2 = kernel v2 instead of v3 (srht_debug_set_kernel)
 extern int g_last_kernel;   // tile kernel of the last srht_sketch* call (bench labels): 1 tiles, 2 ws,

@@ -37,6 +37,8 @@
 // (consumers, before TMEM is released).
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "internal.cuh"
 
 namespace srht {
@@ -750,11 +752,25 @@ __global__ void k_reduce_v3(const __grid_constant__ SketchParams P, const uint32
   const bool second = col >= P.ncols0;
   const ColSrc& cs = second ? P.src[1] : P.src[0];
   const int64_t lc = second ? col - P.ncols0 : col;
-  cs.out[lc * cs.ldo + t] = (float)(sum * P.scale_f64);
+  const float y = (float)(sum * P.scale_f64);
+  cs.out[lc * cs.ldo + t] = y;
+  for (int k = 1; k < P.n_peers; ++k)  // fused gather: the same value into every peer's output (NVLink)
+    P.peers[k][(P.peer_col0 + col) * P.peer_ld + t] = y;
 }
 }  // namespace
 
 namespace {
+// Copy of an r x cols block into peers[1..n) (the peer pointers ride in the parameter block).
+__global__ void k_peer_copy(const float* __restrict__ src, int64_t src_ld, int64_t r, int64_t cols, int n_peers,
+                            int64_t col0, int64_t peer_ld, const __grid_constant__ SketchParams pp) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    if (t >= r) continue;
+    const float v = src[j * src_ld + t];
+    for (int k = 1; k < n_peers; ++k) pp.peers[k][(col0 + j) * peer_ld + t] = v;
+  }
+}
+
 // The same reduction with one CTA per column: slot sums (coalesced partial reads, slabs in
 // order) are placed at their output rows in shared memory, then written out coalesced --
 // k_reduce_v3's stores to rows t scatter 4-byte writes over the column (config 4: step 0.490 ->
@@ -788,9 +804,24 @@ __global__ void __launch_bounds__(512) k_reduce_v3_col(const __grid_constant__ S
     const int64_t lc = second ? col - P.ncols0 : col;
     float* __restrict__ o = cs.out + lc * cs.ldo;
     for (int64_t t = threadIdx.x; t < P.r; t += blockDim.x) o[t] = reinterpret_cast<float*>(red_smem)[t];
+    for (int k = 1; k < P.n_peers; ++k) {  // fused gather: coalesced stores into every peer's output
+      float* __restrict__ po = P.peers[k] + (P.peer_col0 + col) * P.peer_ld;
+      for (int64_t t = threadIdx.x; t < P.r; t += blockDim.x) po[t] = reinterpret_cast<float*>(red_smem)[t];
+    }
   }
 }
 }  // namespace
+
+cudaError_t launch_peer_copy(const float* src, int64_t src_ld, int64_t r, int64_t cols, float* const* peers,
+                             int n_peers, int64_t col0, int64_t peer_ld, cudaStream_t stream) {
+  if (n_peers <= 1 || r <= 0 || cols <= 0) return cudaSuccess;
+  SketchParams pp;
+  memset(&pp, 0, sizeof(pp));
+  for (int k = 0; k < n_peers && k < SRHT_MAX_PEERS; ++k) pp.peers[k] = peers[k];
+  const dim3 grid((unsigned)((r + 255) / 256), (unsigned)(cols < 65535 ? cols : 65535));
+  k_peer_copy<<<grid, 256, 0, stream>>>(src, src_ld, r, cols, n_peers, col0, peer_ld, pp);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_reduce_v3(const SketchParams& sp, const uint32_t* ttab, int rpt, int slab_shift,
                              cudaStream_t stream) {

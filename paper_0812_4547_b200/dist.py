@@ -108,6 +108,87 @@ def sketch_sharded(plan, M_shard, total_cols, group=None, out=None, sketch_fn=No
     return full.t()
 
 
+class _DevArray:
+    """Zero-copy torch view of a library-allocated device buffer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, shape, strides):
+        self.__cuda_array_interface__ = {"shape": shape, "strides": strides, "typestr": "<f4",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+class PeerOutputs:
+    """Every rank's r x c output buffer, mapped into every rank (CUDA IPC), for the fused gather.
+
+    Rank k allocates its own buffer with the library (srht_ipc_alloc), the 64-byte handles are
+    all-gathered over `group`, and each rank maps the others' buffers (srht_ipc_open; peer access
+    over NVLink between GPUs).  `out` is this rank's buffer as a column-major (r, c) float32 tensor.
+    """
+
+    def __init__(self, plan, total_cols, group=None):
+        import ctypes
+        lib = plan._lib
+        self._lib = lib
+        self.r, self.c = plan.r, int(total_cols)
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        nbytes = 4 * self.r * self.c
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        from . import _lib as L
+        L.check(lib.srht_ipc_alloc(nbytes, ctypes.byref(own), handle), "srht_ipc_alloc")
+        self._own = own.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.ptrs = [0] * self.world
+        self._opened = []
+        for k in range(self.world):
+            if k == self.rank:
+                self.ptrs[k] = self._own
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_char * 64).from_buffer_copy(handles[k])
+            L.check(lib.srht_ipc_open(buf, ctypes.byref(p)), "srht_ipc_open")
+            self.ptrs[k] = p.value
+            self._opened.append(p.value)
+        self.out = torch.as_tensor(_DevArray(self._own, (self.r, self.c), (4, 4 * self.r)),
+                                   device=torch.device("cuda", torch.cuda.current_device()))
+
+    def peer_order(self):
+        """Device pointers with this rank's own buffer first (the library's convention)."""
+        return [self.ptrs[self.rank]] + [p for k, p in enumerate(self.ptrs) if k != self.rank]
+
+    def close(self):
+        for p in self._opened:
+            self._lib.srht_ipc_close(p)
+        self._opened = []
+        if self._own:
+            self.out = None
+            self._lib.srht_ipc_free(self._own)
+            self._own = 0
+
+
+def sketch_sharded_p2p(plan, M_shard, total_cols, peers, group=None, workspace=None, host_barrier=False):
+    """Column-shard sketch with the gather fused into the sketch (no NCCL all-gather): this rank's
+    columns are stored straight into every rank's output buffer (PeerOutputs) by the library's
+    reduction kernel over peer memory; one barrier then orders the ranks.  Returns this rank's full
+    (r, total_cols) output (a view of peers.out: the next call overwrites it).
+
+    host_barrier: synchronize the device and use a host barrier (gloo groups); otherwise the NCCL
+    barrier is stream-ordered after the stores.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    c0, c1 = column_range(total_cols, world, rank)
+    if M_shard.shape[1] != c1 - c0:
+        raise ValueError("rank %d expects %d columns, got %d" % (rank, c1 - c0, M_shard.shape[1]))
+    if c1 > c0:
+        plan.sketch_columns_peers(M_shard, c0, peers.peer_order(), plan.r, workspace=workspace)
+    if host_barrier:
+        torch.cuda.synchronize()
+    dist.barrier(group=group)
+    return peers.out
+
+
 def row_range(n, world, rank, granularity):
     """Row shard [r0, r1) of n rows for `rank`: whole multiples of `granularity`, the last
     rank also takes the tail (balanced over granules)."""
