@@ -139,10 +139,74 @@ cudaError_t build_ws_layout(srht_plan* P, const std::vector<int32_t>& K) {
 // the tile buffer (mid layout); ttab: per thread rpt2/2 words holding the output rows t
 // of slots 2i, 2i+1 (bits 0..15, 16..31; 0xffff = empty slot); masks[sh][c] bit q = bit
 // sh of k_mid of slot (q, c).
+//
+// Shared gathers (kernel v3): samples whose k_lo coincide read the same z word.  Thread c's
+// first P3 load slots each feed the accumulator pair (2l, 2l+1) -- two samples with one k_lo,
+// one LDS and one FADD2 with a broadcast operand -- and its remaining rpt - 2 P3 accumulators
+// take one load slot each, so a thread issues rpt - P3 gathers per tile instead of rpt.
+// P3 = rpt/4 when the plan has at least 64 rpt same-k_lo pairs (config 5: 4653 pairs for
+// 4096 needed), else rpt/8, else 0.  Pair rows and single rows are each dealt by bank as in
+// deal_slots.  Returns the accumulator -> sample map acc_t[q*256 + c] and meta[c][l].
+int choose_pairs3(const std::vector<int32_t>& K, int rpt) {
+  if (rpt < 16) return 0;
+  std::vector<int> mult(1 << 14, 0);
+  for (int32_t k : K) ++mult[k & ((1 << 14) - 1)];
+  int64_t avail = 0;
+  for (int m : mult) avail += m / 2;
+  if (avail >= (int64_t)256 * (rpt / 4)) return rpt / 4;
+  if (rpt >= 32 && avail >= (int64_t)256 * (rpt / 8)) return rpt / 8;  // (kernel instantiations)
+  return 0;
+}
+
+void deal_v3_pairs(const std::vector<int32_t>& K, int rpt, int P3, std::vector<int32_t>& acc_t,
+                   std::vector<uint32_t>& meta_off) {
+  const int L = rpt - P3;
+  acc_t.assign((size_t)rpt * 256, -1);
+  meta_off.assign((size_t)256 * L, 0u);
+  std::vector<std::vector<int32_t>> by_lo(1 << 14);
+  for (size_t t = 0; t < K.size(); ++t) by_lo[K[t] & ((1 << 14) - 1)].push_back((int32_t)t);
+  // pairs (by bank of the shared address), then singles (by bank)
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> pb(32);
+  std::vector<std::vector<int32_t>> sb(32);
+  int64_t need = (int64_t)256 * P3;
+  for (int lo = 0; lo < (1 << 14); ++lo) {
+    const std::vector<int32_t>& g = by_lo[lo];
+    const int bank = srht::v3_mid(lo) & 31;
+    size_t i = 0;
+    for (; i + 1 < g.size() && need > 0; i += 2, --need) pb[bank].push_back({g[i], g[i + 1]});
+    for (; i < g.size(); ++i) sb[bank].push_back(g[i]);
+  }
+  // pair rows (l < P3, warp w): row = l * 8 + w; single rows (l >= P3): row = (l - P3) * 8 + w
+  const int prow = P3 * 8, srow = (L - P3) * 8;
+  std::vector<int> pfill(prow > 0 ? prow : 1, 0), sfill(srow > 0 ? srow : 1, 0);
+  int64_t i = 0;
+  for (int b = 0; b < 32; ++b)
+    for (const auto& pr : pb[b]) {
+      const int row = (int)(i++ % prow), lane = pfill[row]++;
+      const int l = row / 8, c = (row % 8) * 32 + lane;
+      acc_t[(size_t)(2 * l) * 256 + c] = pr.first;
+      acc_t[(size_t)(2 * l + 1) * 256 + c] = pr.second;
+      meta_off[(size_t)c * L + l] = (uint32_t)srht::v3_mid(K[pr.first] & ((1 << 14) - 1)) * 4u;
+    }
+  i = 0;
+  for (int b = 0; b < 32; ++b)
+    for (int32_t t : sb[b]) {
+      const int row = (int)(i++ % srow), lane = sfill[row]++;
+      const int l = P3 + row / 8, c = (row % 8) * 32 + lane;
+      acc_t[(size_t)(P3 + l) * 256 + c] = t;  // accumulator 2 P3 + (l - P3)
+      meta_off[(size_t)c * L + l] = (uint32_t)srht::v3_mid(K[t] & ((1 << 14) - 1)) * 4u;
+    }
+}
+
 cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
-  const int rpt = P->rpt2, slots = rpt * 256, mw = rpt / 2;
-  const std::vector<int32_t> slot_t = deal_slots(K, rpt, srht::v3_mid);
-  std::vector<uint32_t> meta((size_t)256 * rpt, 0u);
+  const int rpt = P->rpt2, mw = rpt / 2;
+#ifndef V3_PAIRS
+#define V3_PAIRS 1
+#endif
+  P->pairs3 = V3_PAIRS ? choose_pairs3(K, rpt) : 0;
+  std::vector<int32_t> slot_t;
+  std::vector<uint32_t> meta;
+  deal_v3_pairs(K, rpt, P->pairs3, slot_t, meta);
   std::vector<uint32_t> ttab((size_t)256 * mw, 0xffffffffu);
   std::vector<uint2> masks((size_t)(P->log_j2 > 0 ? P->log_j2 : 1) * 256, make_uint2(0u, 0u));
   for (int q = 0; q < rpt; ++q)
@@ -150,9 +214,7 @@ cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
       const int32_t t = slot_t[q * 256 + c];
       if (t < 0) continue;
       const int k = K[t];
-      const uint32_t off = (uint32_t)srht::v3_mid(k & ((1 << 14) - 1));
       const uint32_t kmid = (uint32_t)(k >> 14) & (uint32_t)(P->J2 - 1);
-      meta[(size_t)c * rpt + q] = off * 4u;  // byte offset in the tile buffer
       uint32_t& tw = ttab[(size_t)c * mw + q / 2];
       tw = (tw & ~(0xffffu << (16 * (q & 1)))) | ((uint32_t)t << (16 * (q & 1)));
       for (int sh = 0; sh < P->log_j2; ++sh)
@@ -344,6 +406,8 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       vp.s_lo32 = (int)s_lo2;
       vp.J32 = (int)vp.J;
       vp.n_sub32 = (int)vp.n_sub;
+      vp.uniform = (s_lo2 + S2) * vp.J <= vp.n_sub ? 1 : 0;
+      vp.pairs = P->pairs3;
       vp.partials = sp.partials;
       vp.trace = srht::g_debug_trace;
       vp.debug = srht::g_debug_mode;

@@ -40,6 +40,7 @@ struct srht_plan {
   // Kernel v3 (TMA-fed, same geometry as v2): layouts for its own tile order.
   bool v3_ok;
   uint4* d_signs3;    // [N/2^14][128] sign bits of rows e + 2p + 256h, bit 2h+e
+  int pairs3;          // kernel v3: load slots per consumer thread that feed two accumulators
   uint32_t* d_meta3;  // [256][rpt2/2]: two 16-bit mid-layout word offsets per word
   uint32_t* d_ttab3;  // [256][rpt2/2]: output rows t of slots (2i, 2i+1), 16 bits each (0xffff: empty)
   uint2* d_masks3;    // [log_j2][256]: bit q = bit sh of k_mid of slot (q, c)
@@ -165,6 +166,8 @@ struct V3Params {
   int64_t J, n_sub, S_act;  // S_act: slabs of this launch, global slabs s_lo ..
   int64_t n_items;        // total_cols * S_act
   int n_items32, S_act32, J32, n_sub32, s_lo32;  // the same, 32-bit (checked on the host)
+  int uniform;            // every slab of the launch is full (J tiles): closed-form tile order
+  int pairs;              // load slots per consumer thread that feed two accumulators (plan pairs3)
   float* partials;        // [S_act][total_cols][rpt2 * 256], slot order (k_reduce_v3 finishes)
   unsigned long long* trace;  // experiment phase timestamps (srht_debug_set_trace), else null
   int debug;                  // experiment knock-outs (srht_debug_set_mode, debug build), else 0

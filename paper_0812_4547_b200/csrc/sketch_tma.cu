@@ -110,7 +110,13 @@ __device__ __forceinline__ float flipf(float x, uint32_t mask) { return __uint_a
 
 template <int CH>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&w)[CH]) {
-  if constexpr (CH == 2) {
+  if constexpr (CH == 16) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]),
+          "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+        : "r"(taddr));
+  } else if constexpr (CH == 2) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(taddr));
   } else if constexpr (CH == 8) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -234,6 +240,13 @@ static_assert(CTRL_SLOTS + NBUF * sizeof(SlotState) <= CTRL_TFULL, "control bloc
 static_assert(CTRL_TFULL + 8 * NQ * NBUF <= CTRL_BYTES, "control block overflows");
 // TMEM columns: [0, 3 x 128) raw tiles of the three buffers (TMEM_RAW), then the consumers' gather offsets
 constexpr int TRAW_COLS = V3_TMEM_RAW ? NBUF * 128 : 0;
+// V3_META_PER_BUF: the gather offsets are held once per tile buffer with the buffer's base already
+// added, so a gather is one LDS [offset + smem base] (no per-sample IMAD of b x BUF_BYTES).
+#ifndef V3_META_PER_BUF
+#define V3_META_PER_BUF 1
+#endif
+constexpr bool META_PER_BUF = V3_META_PER_BUF && !V3_TMEM_RAW;
+__host__ __device__ constexpr int pow2_at_least(int x) { return x <= 32 ? 32 : 2 * pow2_at_least((x + 1) / 2); }
 
 // shared-memory matrix descriptor, no swizzle, K-major canonical layout (8-row core matrices):
 // start address, leading byte offset, stride byte offset 128 (8 rows x 16 B), sm100 version bit
@@ -248,18 +261,40 @@ __device__ __forceinline__ void tile_src(const V3Params& P, const Cursor& c, int
   src = col_ptr(P, c.col) + row0;
 }
 
+// Flat tile f of this CTA when every slab of the launch is full (P.uniform: J tiles per item,
+// no inactive Gray-code steps): item f >> log_j, step f & (J - 1).  False past the last item.
+__device__ __forceinline__ bool flat_tile(const V3Params& P, int f, int& tile, const float*& src, bool& full) {
+  const int it = blockIdx.x + (f >> P.log_j) * gridDim.x;
+  if (it >= P.n_items32) return false;
+  const int col = it / P.S_act32;
+  const int s = P.s_lo32 + it - col * P.S_act32;
+  tile = s * P.J32 + gray(f & (P.J32 - 1));
+  const int64_t row0 = (int64_t)tile * B;
+  full = row0 + B <= P.n;
+  src = col_ptr(P, col) + row0;
+  return true;
+}
+
 template <int DBG>
 __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int b, unsigned char* smem) {
   Cursor c = st.cur;
-  if (c.it >= P.n_items32) return;
+  int tile;
+  const float* src;
+  bool full;
+  const int f_load = st.f;
+#ifndef V3_UNIFORM
+#define V3_UNIFORM 0
+#endif
+  if (V3_UNIFORM && P.uniform) {
+    if (!flat_tile(P, f_load, tile, src, full)) return;
+  } else {
+    if (c.it >= P.n_items32) return;
+    tile_src(P, c, tile, src, full);
+  }
   const Cursor st_loaded = c;
   if ((DBG & 1) && blockIdx.x == 0 && st.f < 4096) P.trace[((size_t)2 * 4096 + st.f) * 8 + 6] = clock64();
   st.f += NBUF;
   const uint32_t bar = smem_u32(smem + CTRL_OFF + 8 * NQ * b);  // quarter q: bar + 8 q
-  int tile;
-  const float* src;
-  bool full;
-  tile_src(P, c, tile, src, full);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
   for (int q = 0; q < NREF; ++q) {  // signs ride with the first part; a tail tile has no data parts
@@ -292,12 +327,17 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
           "l"(reinterpret_cast<const char*>(src) + k * 16384), "r"(bar + 8 * (k * NQ / 4)), "l"(stream)
           : "memory");
   }
-#pragma unroll
-  for (int k = 0; k < NBUF; ++k) cursor_next_active(P, c);
-  st.cur = c;
 #ifndef V3_PFD
 #define V3_PFD 3  // L2 prefetch of the tile V3_PFD active tiles beyond the one just loaded (0: none)
 #endif
+  if (V3_UNIFORM && P.uniform) {
+    if (V3_PFD > 0 && flat_tile(P, f_load + V3_PFD, tile, src, full) && full)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(B * 4) : "memory");
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < NBUF; ++k) cursor_next_active(P, c);
+  st.cur = c;
   if (V3_PFD > 0) {
     Cursor pc = V3_PFD >= NBUF ? c : st_loaded;
 #pragma unroll
@@ -320,15 +360,27 @@ __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int 
   if ((DBG & 1) && blockIdx.x == 0 && (k) < V3_TRACE_TILES)                              \
     P.trace[((size_t)(role) * V3_TRACE_TILES + (k)) * 8 + (pt)] = clock64();
 
-template <int RPT, int DBG>
+// Meta words per TMEM load: the largest of V3_CH, 8, 4, 2 that divides the load slots.
+#ifndef V3_CH
+#define V3_CH 8
+#endif
+__host__ __device__ constexpr int pick_ch(int mw) {
+  return (mw % V3_CH == 0 && mw >= V3_CH) ? V3_CH : (mw % 8 == 0) ? 8 : (mw % 4 == 0) ? 4 : 2;
+}
+
+// RPT accumulators per consumer thread; the first PAIRS load slots each feed an accumulator
+// pair (two samples with the same k_lo: one LDS, one FADD2 with a broadcast operand), the other
+// RPT - 2 PAIRS accumulators one load slot each (plan layout: api.cu deal_v3_pairs).
+template <int RPT, int PAIRS, int DBG>
 __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constant__ V3Params P) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint2* masks_s = reinterpret_cast<uint2*>(smem + MASK_OFF);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CTRL_OFF + CTRL_TMEM);
   SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + CTRL_SLOTS);
-  constexpr int MW = RPT;                            // gather byte offsets (TMEM columns) per consumer thread
+  static_assert(PAIRS % 2 == 0 && 2 * PAIRS <= RPT && (RPT - PAIRS) % 4 == 0, "pair slots");
+  constexpr int MW = RPT - PAIRS;                    // gather byte offsets (TMEM columns) per consumer thread
   // TMEM columns allocated: raw tiles (TMEM_RAW) + gather offsets (two consumer warps per lane quarter)
-  constexpr int TCOLS = V3_TMEM_RAW ? 512 : ((2 * MW) < 32 ? 32 : 2 * MW);
+  constexpr int TCOLS = V3_TMEM_RAW ? 512 : META_PER_BUF ? pow2_at_least(2 * NBUF * MW) : ((2 * MW) < 32 ? 32 : 2 * MW);
   const int tid = threadIdx.x;
 
   // ---------------- setup (all threads) ----------------
@@ -377,13 +429,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
       const uint32_t fullb = smem_u32(smem + CTRL_OFF + 8 * NQ * b);
       mbar_wait(fullb, parity);  // first part (and the signs)
       if (p == 0) { V3_TRACE(g, f, 6) }
-      if (SPLIT && p == 0) {  // quarters 1..3 (data-less for a tail tile)
+#ifndef V3_QSPREAD
+#define V3_QSPREAD 1
+#endif
+      // quarters NREF..3 (data-less for a tail tile): with V3_QSPREAD, lane 0 of warp q of the
+      // group issues quarter q, so no single warp carries all three issues into the group barrier
+      if (SPLIT && (V3_QSPREAD ? ((p & 31) == 0 && (p >> 5) >= NREF) : p == 0)) {
         const bool full_tile = row0 + B <= n;
         uint64_t stream;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const uint32_t dst = smem_u32(buf);
-#pragma unroll
-        for (int q = NREF; q < 4; ++q) {
+        const int q0 = V3_QSPREAD ? (p >> 5) : NREF, q1 = V3_QSPREAD ? (p >> 5) + 1 : 4;
+        for (int q = q0; q < q1; ++q) {
           if (full_tile) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16384;" ::"r"(fullb + 8 * q) : "memory");
             asm volatile(
@@ -553,13 +611,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
     const int wc = c >> 5;
     const uint32_t tbase = *tmem_slot;
     const uint32_t taddr = tbase + ((uint32_t)(32 * (wc & 3)) << 16) + (uint32_t)(TRAW_COLS + (wc >> 2) * MW);
+    // gather offsets of buffer b (META_PER_BUF: one copy per buffer, base added)
+    auto tmeta = [&](int b) -> uint32_t { return META_PER_BUF ? taddr + (uint32_t)(2 * MW * b) : taddr; };
     // meta -> TMEM (once)
 #pragma unroll
     for (int k = 0; k < MW; k += 4) {
       const uint4 m4 = __ldg(reinterpret_cast<const uint4*>(P.meta + (size_t)c * MW + k));
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + k), "r"(m4.x),
-                   "r"(m4.y), "r"(m4.z), "r"(m4.w)
-                   : "memory");
+#pragma unroll
+      for (int b = 0; b < (META_PER_BUF ? NBUF : 1); ++b) {
+        const uint32_t o = META_PER_BUF ? (uint32_t)(b * BUF_BYTES) : 0u;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tmeta(b) + k), "r"(m4.x + o),
+                     "r"(m4.y + o), "r"(m4.z + o), "r"(m4.w + o)
+                     : "memory");
+      }
     }
     // the TMEM stores must complete before the gather loads read the offsets back
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -578,9 +642,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
 #pragma unroll
     for (int q = 0; q < RPT; ++q) acc[q] = 0.f;
     // Gather offsets are the same for every tile, so their TMEM loads run one chunk ahead
-    // across tile boundaries too (an even number of chunks keeps the buffer parity fixed).
-    constexpr int CH = MW >= 16 ? 8 : MW / 2;  // meta words per TMEM load
-    static_assert((MW / CH) % 2 == 0, "even chunk count");
+    // across tile boundaries too (chunk 0 of the next tile lands in w[NCH & 1]; with an odd
+    // chunk count it is moved to w[0] at the end of the tile).
+    constexpr int CH = pick_ch(MW);
+    constexpr int NCH = MW / CH;
+    static_assert(MW % CH == 0 && CH % 2 == 0, "chunking");
     uint32_t w[2][CH];
     tmem_ld<CH>(taddr, w[0]);
     int f = 0;
@@ -594,32 +660,51 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
         if (pp) mk = masks_s[(__ffs(pp) - 1) * NCONS + c];
         if (gray(pp) < cnt) {
           const int b = f % NBUF;
-          const float* buf = reinterpret_cast<const float*>(smem + (size_t)b * BUF_BYTES);
+          const float* buf = reinterpret_cast<const float*>(smem + (META_PER_BUF ? 0 : (size_t)b * BUF_BYTES));
+          const uint32_t tb = tmeta(b), tnext = tmeta(b == NBUF - 1 ? 0 : b + 1);
           if (c == 0) { V3_TRACE(2, f, 0) }
           bar_sync(BAR_READY0 + b, 384);
 #pragma unroll
           for (int k = 0; k < MW; k += CH) {
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             // next chunk in flight (after the last chunk: chunk 0 of the next tile)
-            tmem_ld<CH>(taddr + (k + CH) % MW, w[((k / CH) + 1) & 1]);
+            tmem_ld<CH>(k + CH < MW ? tb + k + CH : tnext, w[((k / CH) + 1) & 1]);
             if (k == 0 && c == 0) { V3_TRACE(2, f, 1) }
             const uint32_t* wk = w[(k / CH) & 1];
 #pragma unroll
             for (int i = 0; i < CH; i += 2) {
-              const int q = k + i;
-              // one byte offset per slot (no address arithmetic); a pair of slots is
-              // accumulated by one FADD2
+              const int l = k + i;  // load slots l, l + 1
+              // one byte offset per slot (no address arithmetic); a pair of accumulators is
+              // updated by one FADD2
               const char* bb = reinterpret_cast<const char*>(buf);
               const float z0 = (DBG & 2) ? __uint_as_float(wk[i] & 0x3fffffffu) : *reinterpret_cast<const float*>(bb + wk[i]);
               const float z1 =
                   (DBG & 2) ? __uint_as_float(wk[i + 1] & 0x3fffffffu) : *reinterpret_cast<const float*>(bb + wk[i + 1]);
-              const uint32_t mw = q < 32 ? mk.x : mk.y;
-              const float2 a = make_float2(flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u),
-                                           flipf(acc[q + 1], __funnelshift_l(mw, mw, 30 - (q & 31)) & 0x80000000u));
-              const float2 sum = __fadd2_rn(a, make_float2(z0, z1));
-              acc[q] = sum.x;
-              acc[q + 1] = sum.y;
+              // frame flip of accumulators q, q+1 (bits q, q+1 of the step's k_mid mask)
+              auto flip2 = [&](int q) {
+                const uint32_t mw = q < 32 ? mk.x : mk.y;
+                return make_float2(flipf(acc[q], __funnelshift_l(mw, mw, 31 - (q & 31)) & 0x80000000u),
+                                   flipf(acc[q + 1], __funnelshift_l(mw, mw, 30 - (q & 31)) & 0x80000000u));
+              };
+              if (l < PAIRS) {  // shared gathers: accumulators (2l, 2l+1) and (2l+2, 2l+3)
+                const float2 s0 = __fadd2_rn(flip2(2 * l), make_float2(z0, z0));
+                const float2 s1 = __fadd2_rn(flip2(2 * l + 2), make_float2(z1, z1));
+                acc[2 * l] = s0.x;
+                acc[2 * l + 1] = s0.y;
+                acc[2 * l + 2] = s1.x;
+                acc[2 * l + 3] = s1.y;
+              } else {  // one accumulator per slot: PAIRS + l, PAIRS + l + 1
+                const int q = PAIRS + l;
+                const float2 sum = __fadd2_rn(flip2(q), make_float2(z0, z1));
+                acc[q] = sum.x;
+                acc[q + 1] = sum.y;
+              }
             }
+          }
+          if constexpr (NCH & 1) {  // the next tile's chunk 0 was loaded into w[1]
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < CH; ++i) w[0][i] = w[1][i];
           }
           if (c == 0) { V3_TRACE(2, f, 2) }
           // the last consumer warp done with buffer b refills it (no consumer-wide barrier)
@@ -691,34 +776,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
   }
 }
 
-template <int RPT, int DBG>
+template <int RPT, int PAIRS, int DBG>
 cudaError_t launch_dbg(const V3Params& vp, int grid, cudaStream_t stream) {
   static std::atomic<uint64_t> attr{0};
-  const cudaError_t e = set_max_dyn_smem_once(k_sketch_tma<RPT, DBG>, SMEM_BYTES, attr);
+  const cudaError_t e = set_max_dyn_smem_once(k_sketch_tma<RPT, PAIRS, DBG>, SMEM_BYTES, attr);
   if (e != cudaSuccess) return e;
-  k_sketch_tma<RPT, DBG><<<grid, NTHREADS, SMEM_BYTES, stream>>>(vp);
+  k_sketch_tma<RPT, PAIRS, DBG><<<grid, NTHREADS, SMEM_BYTES, stream>>>(vp);
   return cudaGetLastError();
 }
-template <int RPT>
-cudaError_t launch_rpt(const V3Params& vp, int grid, cudaStream_t stream) {
+template <int RPT, int PAIRS>
+cudaError_t launch_pairs(const V3Params& vp, int grid, cudaStream_t stream) {
   const int dbg = (vp.trace ? 1 : 0) | (vp.debug << 1);
 #ifdef SRHT_WS_DEBUG
   if constexpr (RPT >= 32) {
     switch (dbg) {
-      case 2: return launch_dbg<RPT, 2>(vp, grid, stream);
-      case 4: return launch_dbg<RPT, 4>(vp, grid, stream);
-      case 6: return launch_dbg<RPT, 6>(vp, grid, stream);
-      case 8: return launch_dbg<RPT, 8>(vp, grid, stream);
-      case 10: return launch_dbg<RPT, 10>(vp, grid, stream);
-      case 12: return launch_dbg<RPT, 12>(vp, grid, stream);
-      case 14: return launch_dbg<RPT, 14>(vp, grid, stream);
-      case 16: return launch_dbg<RPT, 16>(vp, grid, stream);
-      case 18: return launch_dbg<RPT, 18>(vp, grid, stream);
+      case 2: return launch_dbg<RPT, PAIRS, 2>(vp, grid, stream);
+      case 4: return launch_dbg<RPT, PAIRS, 4>(vp, grid, stream);
+      case 6: return launch_dbg<RPT, PAIRS, 6>(vp, grid, stream);
+      case 8: return launch_dbg<RPT, PAIRS, 8>(vp, grid, stream);
+      case 10: return launch_dbg<RPT, PAIRS, 10>(vp, grid, stream);
+      case 12: return launch_dbg<RPT, PAIRS, 12>(vp, grid, stream);
+      case 14: return launch_dbg<RPT, PAIRS, 14>(vp, grid, stream);
+      case 16: return launch_dbg<RPT, PAIRS, 16>(vp, grid, stream);
+      case 18: return launch_dbg<RPT, PAIRS, 18>(vp, grid, stream);
       default: break;
     }
   }
 #endif
-  return dbg & 1 ? launch_dbg<RPT, 1>(vp, grid, stream) : launch_dbg<RPT, 0>(vp, grid, stream);
+  return dbg & 1 ? launch_dbg<RPT, PAIRS, 1>(vp, grid, stream) : launch_dbg<RPT, PAIRS, 0>(vp, grid, stream);
+}
+template <int RPT>
+cudaError_t launch_rpt(const V3Params& vp, int grid, cudaStream_t stream) {
+  if constexpr (RPT >= 16)  // (RPT - PAIRS) % 4 == 0: 16-byte meta rows
+    if (vp.pairs == RPT / 4) return launch_pairs<RPT, RPT / 4>(vp, grid, stream);
+  if constexpr (RPT >= 32)
+    if (vp.pairs == RPT / 8) return launch_pairs<RPT, RPT / 8>(vp, grid, stream);
+  if (vp.pairs == 0) return launch_pairs<RPT, 0>(vp, grid, stream);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace v3
