@@ -968,6 +968,19 @@ int srht_debug_copy_ws_layout(const srht_plan* P, uint32_t* meta, int32_t* perm,
   return 0;
 }
 
+// Undeclared test hook: kernel v3's consumer layout -- load-slot byte offsets meta[c][l]
+// (rpt2 - pairs3 per thread), output rows of the accumulators ttab[c][q/2] (16 bits each), and
+// the number of shared-gather slots pairs3.
+int srht_debug_copy_v3_layout(const srht_plan* P, uint32_t* meta, uint32_t* ttab, int* rpt2, int* pairs3) {
+  if (!P || !P->v3_ok) return 1;
+  *rpt2 = P->rpt2;
+  *pairs3 = P->pairs3;
+  const size_t nm = (size_t)256 * (P->rpt2 - P->pairs3), nt = (size_t)256 * (P->rpt2 / 2);
+  if (meta && cudaMemcpy(meta, P->d_meta3, nm * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return 3;
+  if (ttab && cudaMemcpy(ttab, P->d_ttab3, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return 3;
+  return 0;
+}
+
 // Undeclared experiment hook (scripts only): knock out parts of kernel v2.
 // bit0: producers skip global loads; bit1: consumers skip the gather;
 // bit2: producers skip the butterflies.  Results are wrong when non-zero.

@@ -403,12 +403,21 @@ __global__ void k_gram_reduce(int64_t c, int64_t batch, double* __restrict__ G, 
 // needs once, then issues one DMMA per tile.
 constexpr int SMC = 128, SNT = SMC / 8;  // max columns, max tile rows
 
+// GRAM_DB: the staged rows are double-buffered (dynamic shared memory, 2 x 36 KB): step k+1's
+// rows are written into the other buffer after step k's DMMAs, so one barrier per step.
+#ifndef GRAM_DB
+#define GRAM_DB 1
+#endif
+#ifndef GRAM_SMALL_MINB
+#define GRAM_SMALL_MINB 1
+#endif
 template <bool VEC>
-__global__ void __launch_bounds__(256) k_gram_mma_small(int64_t r, int64_t c, int64_t batch,
+__global__ void __launch_bounds__(256, GRAM_SMALL_MINB) k_gram_mma_small(int64_t r, int64_t c, int64_t batch,
                                                         const float* __restrict__ SM, int64_t ldsm,
                                                         int64_t stride_sm, double* __restrict__ G, int64_t ldg,
                                                         int64_t stride_g) {
-  __shared__ __align__(16) double S[SMC][MPK];
+  extern __shared__ __align__(16) double gsm[];
+  double(*S)[MPK] = reinterpret_cast<double(*)[MPK]>(gsm);
   const int64_t p = blockIdx.x + (int64_t)blockIdx.y * 65535;
   if (p >= batch) return;
   const float* __restrict__ Sp = SM + p * stride_sm;
@@ -444,23 +453,34 @@ __global__ void __launch_bounds__(256) k_gram_mma_small(int64_t r, int64_t c, in
       pf[u] = v;
     }
   };
-  fetch(0);
-  for (int64_t k0 = 0; k0 < r; k0 += MKT) {
+  auto put = [&](double(*D)[MPK]) {
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
       const int idx = tid + 256 * u, cc = idx >> 3, k4 = idx & 7;
       if (cc < cp) {
-        *reinterpret_cast<double2*>(&S[cc][4 * k4]) = make_double2(pf[u].x, pf[u].y);
-        *reinterpret_cast<double2*>(&S[cc][4 * k4 + 2]) = make_double2(pf[u].z, pf[u].w);
+        *reinterpret_cast<double2*>(&D[cc][4 * k4]) = make_double2(pf[u].x, pf[u].y);
+        *reinterpret_cast<double2*>(&D[cc][4 * k4 + 2]) = make_double2(pf[u].z, pf[u].w);
       }
     }
+  };
+  fetch(0);
+  if (GRAM_DB) {
+    put(S);
     __syncthreads();
+  }
+  int cur = 0;
+  for (int64_t k0 = 0; k0 < r; k0 += MKT) {
+    if (!GRAM_DB) {
+      put(S);
+      __syncthreads();
+    }
     if (k0 + MKT < r) fetch(k0 + MKT);
+    const double(*T)[MPK] = S + (GRAM_DB ? cur * SMC : 0);
     if (has_a) {
 #pragma unroll
       for (int kk = 0; kk < MKT; kk += 4) {
-        const double fa = S[8 * ra + gid][kk + tig];
-        const double fb = S[8 * rb + gid][kk + tig];
+        const double fa = T[8 * ra + gid][kk + tig];
+        const double fb = T[8 * rb + gid][kk + tig];
 #pragma unroll
         for (int sl = 0; sl <= SNT; ++sl) {
           int j;
@@ -469,12 +489,16 @@ __global__ void __launch_bounds__(256) k_gram_mma_small(int64_t r, int64_t c, in
           else if (sl >= ra) { j = sl; rowb = false; }
           else { j = rb + sl; rowb = true; }
           if (j >= nt || (rowb && !has_b)) continue;
-          const double fc = S[8 * j + gid][kk + tig];
+          const double fc = T[8 * j + gid][kk + tig];
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                        : "+d"(acc[sl][0]), "+d"(acc[sl][1])
                        : "d"(rowb ? fb : fa), "d"(fc));
         }
       }
+    }
+    if (GRAM_DB) {
+      cur ^= 1;
+      if (k0 + MKT < r) put(S + cur * SMC);  // buffer cur was last read in the previous step
     }
     __syncthreads();
   }
@@ -531,10 +555,15 @@ cudaError_t launch_gram_mma(int64_t r, int64_t c, int64_t batch, const float* SM
   const bool vec = (ldsm % 4 == 0) && (stride_sm % 4 == 0) && ((reinterpret_cast<uintptr_t>(SM) & 15) == 0);
   if (c <= SMC && batch >= 2 * 148) {  // many small problems: one CTA per problem
     const dim3 grid((unsigned)(batch < 65535 ? batch : 65535), (unsigned)((batch + 65534) / 65535));
+    const int smem = (GRAM_DB ? 2 : 1) * SMC * MPK * (int)sizeof(double);
+    static std::atomic<uint64_t> attr_t{0}, attr_f{0};
+    cudaError_t e = vec ? set_max_dyn_smem_once(k_gram_mma_small<true>, smem, attr_t)
+                        : set_max_dyn_smem_once(k_gram_mma_small<false>, smem, attr_f);
+    if (e != cudaSuccess) return e;
     if (vec)
-      k_gram_mma_small<true><<<grid, 256, 0, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g);
+      k_gram_mma_small<true><<<grid, 256, smem, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g);
     else
-      k_gram_mma_small<false><<<grid, 256, 0, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g);
+      k_gram_mma_small<false><<<grid, 256, smem, stream>>>(r, c, batch, SM, ldsm, stride_sm, G, ldg, stride_g);
     return cudaGetLastError();
   }
   int64_t splits, kchunk;

@@ -411,6 +411,54 @@ def test_ws_slot_layout(lib, n, r):
     assert worst <= 2, worst
 
 
+@pytest.mark.parametrize("n,r,want_pairs", [(1 << 26, 16384, 16), (1 << 20, 8192, 4), (1 << 20, 16384, 16),
+                                             (1 << 16, 1024, 0), (1 << 18, 5000, 0)])
+def test_v3_shared_gather_layout(lib, n, r, want_pairs):
+    # Kernel-v3 consumer layout with shared gathers: every sample is an accumulator exactly once;
+    # load slot l < pairs feeds accumulators (2l, 2l+1), which must be two samples with one k_lo;
+    # the others feed accumulator pairs + l; offsets match the mid layout of k_lo; every warp-row
+    # of 32 loads is at most 2-way bank-conflicted.
+    import ctypes
+    from paper_0812_4547_b200 import _lib
+    plan = lib.Plan(n, 1, r, 3)
+    L = _lib.load()
+    rpt, pairs = ctypes.c_int(), ctypes.c_int()
+    assert L.srht_debug_copy_v3_layout(plan._h, None, None, ctypes.byref(rpt), ctypes.byref(pairs)) == 0
+    R, P = rpt.value, pairs.value
+    assert P == want_pairs
+    nl = R - P
+    meta = np.empty(256 * nl, dtype=np.uint32)
+    ttab = np.empty(256 * (R // 2), dtype=np.uint32)
+    assert L.srht_debug_copy_v3_layout(plan._h, meta.ctypes.data, ttab.ctypes.data, ctypes.byref(rpt),
+                                       ctypes.byref(pairs)) == 0
+    meta = meta.reshape(256, nl)
+    tt = ttab.reshape(256, R // 2)
+    acc_t = np.stack([tt & 0xFFFF, tt >> 16], axis=2).reshape(256, R).astype(np.int64)  # [c][q]
+    valid = acc_t != 0xFFFF
+    assert np.array_equal(np.sort(acc_t[valid]), np.arange(r))
+    K = plan.indices().astype(np.int64)
+    lo = K & ((1 << 14) - 1)
+
+    def mid(x):  # kernel v3 z layout
+        return ((x >> 1) & 127) + 130 * ((x & 1) | ((x >> 8) << 1))
+
+    for c in range(256):
+        for l in range(nl):
+            qs = (2 * l, 2 * l + 1) if l < P else (P + l,)
+            ts = [acc_t[c, q] for q in qs if acc_t[c, q] != 0xFFFF]
+            if not ts:
+                continue
+            assert len({int(lo[t]) for t in ts}) == 1, (c, l)
+            assert meta[c, l] == 4 * mid(int(lo[ts[0]])), (c, l)
+    used = np.zeros((256, nl), dtype=bool)
+    for l in range(nl):
+        qs = (2 * l, 2 * l + 1) if l < P else (P + l,)
+        used[:, l] = np.any(valid[:, list(qs)], axis=1)
+    banks = np.where(used, (meta // 4 % 32).astype(np.int64), -1).T.reshape(nl, 8, 32).reshape(-1, 32)
+    worst = max(np.bincount(row[row >= 0], minlength=32).max() if (row >= 0).any() else 0 for row in banks)
+    assert worst <= 2, worst
+
+
 # ---- row shards: unscaled FP64 partials per shard, summed by the caller ----
 
 def _row_cuts(n, g, k):
