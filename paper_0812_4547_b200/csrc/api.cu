@@ -271,6 +271,7 @@ srht::SketchParams base_params(const srht_plan* P) {
   sp.signs = reinterpret_cast<const uint32_t*>(P->d_signs);
   sp.words32 = P->words64 * 2;
   sp.K = P->d_K;
+  sp.colk = P->d_colk;
   sp.r = P->r;
   sp.n = P->n;
   sp.J = P->J;
@@ -610,6 +611,38 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
     }
     P->v3_ok = (e == cudaSuccess) && P->log_j2 <= srht::V3_MAX_LOGJ && P->r < 0xffff;  // 16-bit t table
   }
+  // Whole-column kernel gather order (FP32 plans with N_eff = 2^13, r <= 1024): per problem, the
+  // kept rows sorted by the bank of their y words (tile word lo + 1024 j at pad(lo) + 1056 j, bank
+  // (lo + lo / 32) mod 32) and dealt round-robin over the warp-wide steps of 32 entries.
+#ifndef COL_PRUNE
+#define COL_PRUNE 1
+#endif
+  if (COL_PRUNE && e == cudaSuccess && !(flags & SRHT_PLAN_ACCUM_FP64) && P->N_eff == (1 << 13) && r <= 1024) {
+    std::vector<int32_t> Kall((size_t)batch * r);
+    e = cudaMemcpy(Kall.data(), P->d_K, Kall.size() * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    std::vector<uint32_t> ck(Kall.size());
+    const int rows = (int)((r + 31) / 32);
+    std::vector<std::vector<int32_t>> bk(32);
+    std::vector<int> fill(rows);
+    for (int64_t pb = 0; e == cudaSuccess && pb < batch; ++pb) {
+      const int32_t* Kp = Kall.data() + pb * r;
+      for (auto& v : bk) v.clear();
+      for (int t = 0; t < r; ++t) {
+        const int lo = Kp[t] & 1023;
+        bk[(lo + (lo >> 5)) & 31].push_back(t);
+      }
+      std::fill(fill.begin(), fill.end(), 0);
+      int64_t i = 0;
+      uint32_t* out = ck.data() + pb * r;
+      for (int b = 0; b < 32; ++b)
+        for (int32_t t : bk[b]) {
+          int row = (int)(i++ % rows);
+          while (fill[row] >= 32 || (int64_t)row * 32 + fill[row] >= r) row = (row + 1) % rows;  // last row short
+          out[(size_t)row * 32 + fill[row]++] = (uint32_t)Kp[t] | ((uint32_t)t << 16);
+        }
+    }
+    if (e == cudaSuccess) e = upload(&P->d_colk, ck);
+  }
   // FP64 TMA kernel geometry (FP64 plans, single problem): B = 2^12, G sample groups of up to
   // 8192 samples (32 FP64 accumulators per consumer thread), slabs of up to 512 tiles, shortened
   // until the (group, column, slab) items give ~6 per SM.
@@ -672,6 +705,7 @@ srht_status srht_plan_destroy(srht_plan* P) {
   cudaFree(P->d_meta64);
   cudaFree(P->d_ttab64);
   cudaFree(P->d_masks64);
+  cudaFree(P->d_colk);
   delete P;
   return SRHT_OK;
 }

@@ -41,7 +41,7 @@ struct srht_plan {
   bool v3_ok;
   uint4* d_signs3;    // [N/2^14][128] sign bits of rows e + 2p + 256h, bit 2h+e
   int pairs3;          // kernel v3: load slots per consumer thread that feed two accumulators
-  uint32_t* d_meta3;  // [256][rpt2/2]: two 16-bit mid-layout word offsets per word
+  uint32_t* d_meta3;  // [256][rpt2 - pairs3]: byte offset of load slot l's z value (mid layout)
   uint32_t* d_ttab3;  // [256][rpt2/2]: output rows t of slots (2i, 2i+1), 16 bits each (0xffff: empty)
   uint2* d_masks3;    // [log_j2][256]: bit q = bit sh of k_mid of slot (q, c)
   // FP64-accumulation TMA kernel (sketch_tma64.cu; FP64 plans, single problem, N >= 2^12,
@@ -54,6 +54,9 @@ struct srht_plan {
   uint32_t* d_meta64; // [G][256][rpt64]: byte offset of slot (q, c)'s z value (mid layout)
   int32_t* d_ttab64;  // [G][256][rpt64]: output row t of the slot, -1 if empty
   uint32_t* d_masks64;// [G][log_j64][256]: bit q = bit l of k_mid of slot (q, c)
+  // Whole-column kernel (N_eff = 2^13, r <= 1024): per problem the kept rows in gather order,
+  // k | (output row t) << 16, dealt so the 32 entries of a warp-wide step hit distinct banks.
+  uint32_t* d_colk;   // [batch][r]
 };
 
 namespace srht {
@@ -120,6 +123,7 @@ struct SketchParams {
   float* peers[SRHT_MAX_PEERS];
   int n_peers;
   int64_t peer_col0, peer_ld;
+  const uint32_t* colk;       // whole-column kernel: plan d_colk (null: full last round + gather)
 };
 // FP64-accumulation parity mode (sketch_f64.cu), v1 slab geometry.
 cudaError_t launch_sketch_f64(const srht_plan* P, const SketchParams& sp, cudaStream_t stream);

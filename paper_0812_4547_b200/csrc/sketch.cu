@@ -389,7 +389,10 @@ __device__ __align__(128) float g_col_zeros[COL_N + COL_N / 32];
 #define COL_TMA_ZERO 1
 #endif
 
-__global__ void __launch_bounds__(COL_T) k_sketch_col(const __grid_constant__ SketchParams P) {
+#ifndef COL_MINB
+#define COL_MINB 6
+#endif
+__global__ void __launch_bounds__(COL_T, COL_MINB) k_sketch_col(const __grid_constant__ SketchParams P) {
   __shared__ __align__(16) float tile[COL_N + COL_N / 32];
   const int tid = threadIdx.x;
   const int64_t col = blockIdx.x + (int64_t)blockIdx.y * 65535;
@@ -466,6 +469,46 @@ __global__ void __launch_bounds__(COL_T) k_sketch_col(const __grid_constant__ Sk
     }
   }
   __syncthreads();
+  if (P.colk && P.r <= 4 * COL_T) {
+    // ---- pruned last three row bits: only the kept rows of z are formed.  Kept row
+    // k = lo | hi << 10 needs z[k] = sum_j (-1)^popc(hi & j) y[lo + 1024 j] (y = the tile after
+    // rounds A and B): eight reads and seven adds instead of round C over all 8192 rows plus the
+    // gather.  The plan's gather order (d_colk) puts 32 distinct banks in each warp-wide step. ----
+    const uint32_t* __restrict__ ck = P.colk + prob * P.r;
+    float zr[4];
+    int zd[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = tid + COL_T * q;
+      zd[q] = -1;
+      zr[q] = 0.f;
+      if (i < P.r) {
+        const uint32_t w = __ldg(ck + i);
+        const int k = (int)(w & 0xffffu), lo = k & 1023;
+        const uint32_t hi = (uint32_t)k >> 10;
+        const float* y = tile + cpad(lo);  // y[lo + 1024 j] at offset 1056 j
+        const uint32_t s0 = (hi & 1u) << 31, s1 = ((hi >> 1) & 1u) << 31, s2 = (hi >> 2) << 31;
+        const float2 a = __fadd2_rn(make_float2(y[0], y[4 * 1056]),
+                                    make_float2(__uint_as_float(__float_as_uint(y[1056]) ^ s0),
+                                                __uint_as_float(__float_as_uint(y[5 * 1056]) ^ s0)));
+        const float2 b = __fadd2_rn(make_float2(y[2 * 1056], y[6 * 1056]),
+                                    make_float2(__uint_as_float(__float_as_uint(y[3 * 1056]) ^ s0),
+                                                __uint_as_float(__float_as_uint(y[7 * 1056]) ^ s0)));
+        const float2 c = __fadd2_rn(a, make_float2(__uint_as_float(__float_as_uint(b.x) ^ s1),
+                                                   __uint_as_float(__float_as_uint(b.y) ^ s1)));
+        zr[q] = c.x + __uint_as_float(__float_as_uint(c.y) ^ s2);
+        zd[q] = (int)(w >> 16);
+      }
+    }
+    __syncthreads();  // every y read before z overwrites the tile
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (zd[q] >= 0) tile[zd[q]] = zr[q];
+    __syncthreads();
+    float* __restrict__ o = cs.out + lc * cs.ldo;
+    for (int64_t t = tid; t < P.r; t += COL_T) o[t] = tile[t] * P.scale;
+    return;
+  }
   // ---- round C: bits 10..12 (u bits 0..2) with bits 0, 1 carried along (u bits 3, 4);
   // thread = bits 2..9.  x = f + 4 tid + 1024 g, u = g + 8 f ----
   {

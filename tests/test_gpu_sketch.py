@@ -121,6 +121,33 @@ def test_integer_inputs_bit_exact(lib, n, r):
     assert np.array_equal(SM, ref)
 
 
+@pytest.mark.parametrize("n,r", [(8192, 1024), (5000, 256), (8192, 1000)])
+def test_column_kernel_integer_bit_exact(lib, n, r):
+    # Whole-column kernel (N = 2^13): with r <= 1024 the last three row bits are evaluated only at
+    # the kept rows (plan gather order); integer inputs keep every sum exact, so the batched sketch
+    # must equal the oracle's bit for bit (r = 1000 is not a power of 4: compare with the same
+    # FP32 scale applied).
+    from oracle import srht as osr
+    batch, c = 12, 100  # >= 1184 columns: one slab per column (the column kernel's condition)
+    rng = np.random.default_rng(n + r)
+    amax = max(1, (1 << 23) // n)
+    M = rng.integers(-amax, amax + 1, size=(n, batch * c)).astype(np.float32)
+    M[rng.random(M.shape) < 0.95] = 0.0  # sparse CSC input (the batched CSC path runs the column kernel)
+    colptr = np.concatenate([[0], np.cumsum((M != 0).sum(axis=0))]).astype(np.int64)
+    rows = np.concatenate([np.flatnonzero(M[:, j]) for j in range(M.shape[1])]).astype(np.int32)
+    vals = np.concatenate([M[M[:, j] != 0, j] for j in range(M.shape[1])]).astype(np.float32)
+    plan = lib.Plan(n, c - 1, r, 17, batch=batch)
+    out = plan.sketch_batched(_csc_dev(colptr, rows, vals, (n, batch * c))).cpu().numpy().astype(np.float64)
+    assert lib.library().srht_debug_last_kernel() == 5
+    scale = float(np.float32(1.0 / np.sqrt(r)))
+    for p in range(batch):
+        ref = osr.sketch(M[:, p * c:(p + 1) * c].astype(np.float64), 17, r, p=p)  # r^{-1/2} sum
+        unscaled = ref * np.sqrt(r)  # exact integers
+        assert np.allclose(unscaled, np.round(unscaled), atol=1e-6)
+        want = (np.round(unscaled).astype(np.float32) * np.float32(scale)).astype(np.float64)
+        assert np.array_equal(out[p].T, want)
+
+
 def test_single_nonzero_closed_form(lib):
     from oracle import srht as osr
     n, r, seed = 20000, 1024, 3
