@@ -390,7 +390,7 @@ __device__ __align__(128) float g_col_zeros[COL_N + COL_N / 32];
 #endif
 
 #ifndef COL_MINB
-#define COL_MINB 6
+#define COL_MINB 5
 #endif
 __global__ void __launch_bounds__(COL_T, COL_MINB) k_sketch_col(const __grid_constant__ SketchParams P) {
   __shared__ __align__(16) float tile[COL_N + COL_N / 32];
@@ -404,21 +404,45 @@ __global__ void __launch_bounds__(COL_T, COL_MINB) k_sketch_col(const __grid_con
   const uint32_t* __restrict__ signs = P.signs + prob * P.words32;
   const int32_t* __restrict__ Kp = P.K + prob * P.r;
   const int n = (int)P.n;
+  // kept rows of the pruned last three bits (plan gather order), loaded now: their latency is
+  // hidden behind the tile's fill and rounds A and B
+  const bool pruned = P.colk && P.r <= 4 * COL_T;
+  uint32_t ckw[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = tid + COL_T * q;
+    ckw[q] = (pruned && i < P.r) ? __ldg(P.colk + prob * P.r + i) : 0xffffffffu;
+  }
   // ---- D x into the padded tile (rows >= n stay 0) ----
   if (cs.fmt == SRHT_CSC) {
+    // The zero fill (bulk copy from a zeroed L2-resident buffer: no LSU wavefronts) is issued
+    // first, and each thread's first CSC entry (row, value, neighbours' rows, sign word) is
+    // loaded while it lands, so the two latencies overlap.
+    __shared__ __align__(8) uint64_t zbar;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&zbar);
+    if (COL_TMA_ZERO && tid == 0) {
+      constexpr uint32_t bytes = (COL_N + COL_N / 32) * 4;
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(tile)),
+                   "l"(g_col_zeros), "r"(bytes), "r"(bar)
+                   : "memory");
+    }
+    const int64_t cbeg = cs.colptr[lc], cend = cs.colptr[lc + 1];
+    const int64_t e0 = cbeg + tid;
+    int r0 = -1, rprev = -1, rnext = -1;
+    float v0 = 0.f;
+    uint32_t sw0 = 0u;
+    if (e0 < cend) {
+      r0 = cs.rowidx[e0];
+      v0 = cs.vals[e0];
+      if (e0 > cbeg) rprev = cs.rowidx[e0 - 1];
+      if (e0 + 1 < cend) rnext = cs.rowidx[e0 + 1];
+      sw0 = __ldg(signs + (r0 >> 5));
+    }
     if (COL_TMA_ZERO) {
-      __shared__ __align__(8) uint64_t zbar;
-      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&zbar);
-      if (tid == 0) {
-        constexpr uint32_t bytes = (COL_N + COL_N / 32) * 4;
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(tile)),
-                     "l"(g_col_zeros), "r"(bytes), "r"(bar)
-                     : "memory");
-      }
       __syncthreads();  // the barrier is initialised before anyone waits on it
       asm volatile(
           "{\n .reg .pred P;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n @!P bra W_%=;\n}" ::"r"(bar)
@@ -428,11 +452,23 @@ __global__ void __launch_bounds__(COL_T, COL_MINB) k_sketch_col(const __grid_con
         reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncthreads();
     }
-    const int64_t cend = cs.colptr[lc + 1];
-    for (int64_t e = cs.colptr[lc] + tid; e < cend; e += COL_T) {
+    // scatter D x: rows are sorted within a column, so duplicates are adjacent; the first entry of
+    // each run of equal rows sums the run (in entry order: deterministic) and stores it once.
+    // (Shared FP32 atomicAdd compiles to a CAS loop: ncu put 13% of this kernel's shared-memory
+    // wavefronts in it.)
+    if (e0 < cend && rprev != r0) {
+      float v = v0;
+      if (rnext == r0)
+        for (int64_t e2 = e0 + 1; e2 < cend && cs.rowidx[e2] == r0; ++e2) v += cs.vals[e2];
+      tile[cpad(r0)] = flip(v, (sw0 >> (r0 & 31)) & 1u);
+    }
+    for (int64_t e = e0 + COL_T; e < cend; e += COL_T) {
       const int row = cs.rowidx[e];
+      if (cs.rowidx[e - 1] == row) continue;  // not the first of its run
+      float v = cs.vals[e];
+      for (int64_t e2 = e + 1; e2 < cend && cs.rowidx[e2] == row; ++e2) v += cs.vals[e2];
       const uint32_t sb = (__ldg(signs + (row >> 5)) >> (row & 31)) & 1u;
-      atomicAdd(&tile[cpad(row)], flip(cs.vals[e], sb));  // duplicates are summed
+      tile[cpad(row)] = flip(v, sb);
     }
   } else {
     const float* __restrict__ colp = cs.vals + lc * cs.ld;
@@ -469,21 +505,19 @@ __global__ void __launch_bounds__(COL_T, COL_MINB) k_sketch_col(const __grid_con
     }
   }
   __syncthreads();
-  if (P.colk && P.r <= 4 * COL_T) {
+  if (pruned) {
     // ---- pruned last three row bits: only the kept rows of z are formed.  Kept row
     // k = lo | hi << 10 needs z[k] = sum_j (-1)^popc(hi & j) y[lo + 1024 j] (y = the tile after
     // rounds A and B): eight reads and seven adds instead of round C over all 8192 rows plus the
     // gather.  The plan's gather order (d_colk) puts 32 distinct banks in each warp-wide step. ----
-    const uint32_t* __restrict__ ck = P.colk + prob * P.r;
     float zr[4];
     int zd[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int i = tid + COL_T * q;
       zd[q] = -1;
       zr[q] = 0.f;
-      if (i < P.r) {
-        const uint32_t w = __ldg(ck + i);
+      if (ckw[q] != 0xffffffffu) {
+        const uint32_t w = ckw[q];
         const int k = (int)(w & 0xffffu), lo = k & 1023;
         const uint32_t hi = (uint32_t)k >> 10;
         const float* y = tile + cpad(lo);  // y[lo + 1024 j] at offset 1056 j
