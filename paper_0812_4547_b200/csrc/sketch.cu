@@ -102,7 +102,10 @@ __host__ __device__ constexpr bool meta_in_smem() { return V1_META_SMEM && RPT =
 #define V1_THREADS_PER_SM 512
 #endif
 template <int LOG_B, int RPT>
-__global__ void __launch_bounds__((1 << LOG_B) / 32, (meta_in_smem<RPT>() ? V1_THREADS_PER_SM : 512) / ((1 << LOG_B) / 32))
+#ifndef V1_TPS_OTHER
+#define V1_TPS_OTHER 512  // threads per SM the register budget targets when RPT != 32
+#endif
+__global__ void __launch_bounds__((1 << LOG_B) / 32, (meta_in_smem<RPT>() ? V1_THREADS_PER_SM : V1_TPS_OTHER) / ((1 << LOG_B) / 32))
     k_sketch_tiles(const __grid_constant__ SketchParams P) {
   constexpr int B = 1 << LOG_B;
   constexpr int T = B / 32;
