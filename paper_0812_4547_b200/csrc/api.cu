@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -612,34 +613,45 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
     P->v3_ok = (e == cudaSuccess) && P->log_j2 <= srht::V3_MAX_LOGJ && P->r < 0xffff;  // 16-bit t table
   }
   // Whole-column kernel gather order (FP32 plans with N_eff = 2^13, r <= 1024): per problem, the
-  // kept rows sorted by the bank of their y words (tile word lo + 1024 j at pad(lo) + 1056 j, bank
-  // (lo + lo / 32) mod 32) and dealt round-robin over the warp-wide steps of 32 entries.
+  // kept rows are placed in SRHT_COL_SLOTS = 40 warp-wide steps of 32 slots (5 per thread), each
+  // step taking at most one kept row per bank of its y words (tile word lo + 1024 j at
+  // pad(lo) + 1056 j: bank (lo + lo / 32) mod 32) and, where possible, one per bank of its staging
+  // word t (t mod 32) -- greedy, rows scanned for the fewest repeats.  Host simulation on config 2's
+  // plans: 398 shared wavefronts per column for the gathers and z stores vs 594 with 32 steps.
 #ifndef COL_PRUNE
 #define COL_PRUNE 1
 #endif
   if (COL_PRUNE && e == cudaSuccess && !(flags & SRHT_PLAN_ACCUM_FP64) && P->N_eff == (1 << 13) && r <= 1024) {
     std::vector<int32_t> Kall((size_t)batch * r);
     e = cudaMemcpy(Kall.data(), P->d_K, Kall.size() * sizeof(int32_t), cudaMemcpyDeviceToHost);
-    std::vector<uint32_t> ck(Kall.size());
-    const int rows = (int)((r + 31) / 32);
-    std::vector<std::vector<int32_t>> bk(32);
-    std::vector<int> fill(rows);
+    constexpr int ROWS = srht::COL_SLOTS / 32;
+    std::vector<uint32_t> ck((size_t)batch * srht::COL_SLOTS, 0xffffffffu);
+    std::vector<std::pair<int, int32_t>> order(r);
     for (int64_t pb = 0; e == cudaSuccess && pb < batch; ++pb) {
       const int32_t* Kp = Kall.data() + pb * r;
-      for (auto& v : bk) v.clear();
       for (int t = 0; t < r; ++t) {
         const int lo = Kp[t] & 1023;
-        bk[(lo + (lo >> 5)) & 31].push_back(t);
+        order[t] = {(lo + (lo >> 5)) & 31, t};
       }
-      std::fill(fill.begin(), fill.end(), 0);
-      int64_t i = 0;
-      uint32_t* out = ck.data() + pb * r;
-      for (int b = 0; b < 32; ++b)
-        for (int32_t t : bk[b]) {
-          int row = (int)(i++ % rows);
-          while (fill[row] >= 32 || (int64_t)row * 32 + fill[row] >= r) row = (row + 1) % rows;  // last row short
-          out[(size_t)row * 32 + fill[row]++] = (uint32_t)Kp[t] | ((uint32_t)t << 16);
+      std::sort(order.begin(), order.begin() + r);
+      int cnt_a[ROWS][32] = {}, cnt_b[ROWS][32] = {}, fill[ROWS] = {};
+      uint32_t* out = ck.data() + pb * srht::COL_SLOTS;
+      for (int m = 0; m < r; ++m) {
+        const int a = order[m].first, t = order[m].second, b = t & 31;
+        int best = -1;
+        long long bs = 0;
+        for (int row = 0; row < ROWS; ++row) {
+          if (fill[row] >= 32) continue;
+          const long long sc = (long long)cnt_a[row][a] * 1000000 + cnt_b[row][b] * 1000 + fill[row];
+          if (best < 0 || sc < bs) {
+            best = row;
+            bs = sc;
+          }
         }
+        ++cnt_a[best][a];
+        ++cnt_b[best][b];
+        out[(size_t)best * 32 + fill[best]++] = (uint32_t)Kp[t] | ((uint32_t)t << 16);
+      }
     }
     if (e == cudaSuccess) e = upload(&P->d_colk, ck);
   }

@@ -55,11 +55,13 @@ struct srht_plan {
   int32_t* d_ttab64;  // [G][256][rpt64]: output row t of the slot, -1 if empty
   uint32_t* d_masks64;// [G][log_j64][256]: bit q = bit l of k_mid of slot (q, c)
   // Whole-column kernel (N_eff = 2^13, r <= 1024): per problem the kept rows in gather order,
-  // k | (output row t) << 16, dealt so the 32 entries of a warp-wide step hit distinct banks.
-  uint32_t* d_colk;   // [batch][r]
+  // k | (output row t) << 16 (0xffffffff: empty slot), in srht::COL_SLOTS slots = 40 warp-wide
+  // steps of 32, dealt so a step's gathers (and where possible its staging stores) hit distinct banks.
+  uint32_t* d_colk;   // [batch][COL_SLOTS]
 };
 
 namespace srht {
+constexpr int COL_SLOTS = 5 * 256;  // whole-column kernel: kept-row slots per problem (5 per thread)
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) holds per device: set it once per device
 // a kernel runs on (bit per device ordinal), safely from several host threads.

@@ -409,13 +409,12 @@ __global__ void __launch_bounds__(COL_T, COL_MINB) k_sketch_col(const __grid_con
   const int n = (int)P.n;
   // kept rows of the pruned last three bits (plan gather order), loaded now: their latency is
   // hidden behind the tile's fill and rounds A and B
+  constexpr int ZPT = COL_SLOTS / COL_T;  // kept-row slots per thread
   const bool pruned = P.colk && P.r <= 4 * COL_T;
-  uint32_t ckw[4];
+  uint32_t ckw[ZPT];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = tid + COL_T * q;
-    ckw[q] = (pruned && i < P.r) ? __ldg(P.colk + prob * P.r + i) : 0xffffffffu;
-  }
+  for (int q = 0; q < ZPT; ++q)
+    ckw[q] = pruned ? __ldg(P.colk + prob * COL_SLOTS + tid + COL_T * q) : 0xffffffffu;
   // ---- D x into the padded tile (rows >= n stay 0) ----
   if (cs.fmt == SRHT_CSC) {
     // The zero fill (bulk copy from a zeroed L2-resident buffer: no LSU wavefronts) is issued
@@ -512,11 +511,12 @@ __global__ void __launch_bounds__(COL_T, COL_MINB) k_sketch_col(const __grid_con
     // ---- pruned last three row bits: only the kept rows of z are formed.  Kept row
     // k = lo | hi << 10 needs z[k] = sum_j (-1)^popc(hi & j) y[lo + 1024 j] (y = the tile after
     // rounds A and B): eight reads and seven adds instead of round C over all 8192 rows plus the
-    // gather.  The plan's gather order (d_colk) puts 32 distinct banks in each warp-wide step. ----
-    float zr[4];
-    int zd[4];
+    // gather.  The plan's gather order (d_colk, 5 slots per thread) puts distinct banks in each
+    // warp-wide step where the bank counts allow. ----
+    float zr[ZPT];
+    int zd[ZPT];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < ZPT; ++q) {
       zd[q] = -1;
       zr[q] = 0.f;
       if (ckw[q] != 0xffffffffu) {
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(COL_T, COL_MINB) k_sketch_col(const __grid_con
     }
     __syncthreads();  // every y read before z overwrites the tile
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < ZPT; ++q)
       if (zd[q] >= 0) tile[zd[q]] = zr[q];
     __syncthreads();
     float* __restrict__ o = cs.out + lc * cs.ldo;

@@ -3,7 +3,7 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out/n23
 mkdir -p $O
-for C in 2 3; do
+for C in ${CFGS:-2 3}; do
   K=$([ $C = 2 ] && echo k_sketch_col || echo k_sketch_tiles)
   CMD="python bench.py --config $C --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
   timeout 600 $CMD > $O/plain_c$C.log 2>&1 && \
