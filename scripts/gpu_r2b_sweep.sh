@@ -3,7 +3,7 @@
 # tests, smoke, bench lines for every config and mode (the default line as the driver runs it),
 # Algorithm-1 stage timings, the config-4 end-to-end gate, drift and the ncu launch list.
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/sw2
+O=gpurun_out/${SWDIR:-sw2}
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
