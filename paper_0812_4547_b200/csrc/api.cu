@@ -199,6 +199,38 @@ void deal_v3_pairs(const std::vector<int32_t>& K, int rpt, int P3, std::vector<i
     }
 }
 
+// Whole-column kernel gather order for one problem (r <= 1024 kept rows K, N = 2^13): out[COL_SLOTS]
+// = k | t << 16 (0xffffffff: empty) in 40 warp-wide steps of 32 slots; each kept row goes to the
+// step with the fewest kept rows of its gather bank (lo + lo / 32) mod 32 so far, then the fewest
+// of its staging bank t mod 32, then the fewest entries.
+void deal_col_slots(const int32_t* K, int r, uint32_t* out) {
+  constexpr int ROWS = srht::COL_SLOTS / 32;
+  std::vector<std::pair<int, int32_t>> order(r);
+  for (int t = 0; t < r; ++t) {
+    const int lo = K[t] & 1023;
+    order[t] = {(lo + (lo >> 5)) & 31, t};
+  }
+  std::sort(order.begin(), order.end());
+  int cnt_a[ROWS][32] = {}, cnt_b[ROWS][32] = {}, fill[ROWS] = {};
+  for (int i = 0; i < srht::COL_SLOTS; ++i) out[i] = 0xffffffffu;
+  for (int m = 0; m < r; ++m) {
+    const int a = order[m].first, t = order[m].second, b = t & 31;
+    int best = -1;
+    long long bs = 0;
+    for (int row = 0; row < ROWS; ++row) {
+      if (fill[row] >= 32) continue;
+      const long long sc = (long long)cnt_a[row][a] * 1000000 + cnt_b[row][b] * 1000 + fill[row];
+      if (best < 0 || sc < bs) {
+        best = row;
+        bs = sc;
+      }
+    }
+    ++cnt_a[best][a];
+    ++cnt_b[best][b];
+    out[(size_t)best * 32 + fill[best]++] = (uint32_t)K[t] | ((uint32_t)t << 16);
+  }
+}
+
 cudaError_t build_v3_layout(srht_plan* P, const std::vector<int32_t>& K) {
   const int rpt = P->rpt2, mw = rpt / 2;
 #ifndef V3_PAIRS
@@ -624,35 +656,9 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
   if (COL_PRUNE && e == cudaSuccess && !(flags & SRHT_PLAN_ACCUM_FP64) && P->N_eff == (1 << 13) && r <= 1024) {
     std::vector<int32_t> Kall((size_t)batch * r);
     e = cudaMemcpy(Kall.data(), P->d_K, Kall.size() * sizeof(int32_t), cudaMemcpyDeviceToHost);
-    constexpr int ROWS = srht::COL_SLOTS / 32;
     std::vector<uint32_t> ck((size_t)batch * srht::COL_SLOTS, 0xffffffffu);
-    std::vector<std::pair<int, int32_t>> order(r);
-    for (int64_t pb = 0; e == cudaSuccess && pb < batch; ++pb) {
-      const int32_t* Kp = Kall.data() + pb * r;
-      for (int t = 0; t < r; ++t) {
-        const int lo = Kp[t] & 1023;
-        order[t] = {(lo + (lo >> 5)) & 31, t};
-      }
-      std::sort(order.begin(), order.begin() + r);
-      int cnt_a[ROWS][32] = {}, cnt_b[ROWS][32] = {}, fill[ROWS] = {};
-      uint32_t* out = ck.data() + pb * srht::COL_SLOTS;
-      for (int m = 0; m < r; ++m) {
-        const int a = order[m].first, t = order[m].second, b = t & 31;
-        int best = -1;
-        long long bs = 0;
-        for (int row = 0; row < ROWS; ++row) {
-          if (fill[row] >= 32) continue;
-          const long long sc = (long long)cnt_a[row][a] * 1000000 + cnt_b[row][b] * 1000 + fill[row];
-          if (best < 0 || sc < bs) {
-            best = row;
-            bs = sc;
-          }
-        }
-        ++cnt_a[best][a];
-        ++cnt_b[best][b];
-        out[(size_t)best * 32 + fill[best]++] = (uint32_t)Kp[t] | ((uint32_t)t << 16);
-      }
-    }
+    for (int64_t pb = 0; e == cudaSuccess && pb < batch; ++pb)
+      deal_col_slots(Kall.data() + pb * r, (int)r, ck.data() + pb * srht::COL_SLOTS);
     if (e == cudaSuccess) e = upload(&P->d_colk, ck);
   }
   // FP64 TMA kernel geometry (FP64 plans, single problem): B = 2^12, G sample groups of up to
@@ -1011,6 +1017,25 @@ int srht_debug_copy_ws_layout(const srht_plan* P, uint32_t* meta, int32_t* perm,
     return 3;
   if (perm && cudaMemcpy(perm, P->d_perm, P->rpt2 * 256 * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
     return 3;
+  return 0;
+}
+
+// Undeclared host-only test hooks (no CUDA calls; `-m "not gpu"` tests run them on the oracle's
+// plans): the slot dealing of kernel v3 (shared gathers) and of the whole-column kernel.
+int srht_debug_deal_v3(const int32_t* K, int64_t r, int rpt, int* pairs, int32_t* acc_t, uint32_t* meta) {
+  if (!K || r < 1 || r > 256 * (int64_t)rpt || !pairs || !acc_t || !meta) return 1;
+  const std::vector<int32_t> Kv(K, K + r);
+  *pairs = choose_pairs3(Kv, rpt);
+  std::vector<int32_t> a;
+  std::vector<uint32_t> m;
+  deal_v3_pairs(Kv, rpt, *pairs, a, m);
+  std::copy(a.begin(), a.end(), acc_t);
+  std::copy(m.begin(), m.end(), meta);
+  return 0;
+}
+int srht_debug_deal_col(const int32_t* K, int64_t r, uint32_t* out) {
+  if (!K || r < 1 || r > 1024 || !out) return 1;
+  deal_col_slots(K, (int)r, out);
   return 0;
 }
 
