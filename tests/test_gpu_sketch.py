@@ -68,6 +68,8 @@ def last_kernel(lib):
     (5000, 3, 700, 15, V1),         # N = 2^13, few columns: short slabs, v1
     (8192, 2, 8192, 16, COL),       # N = 2^13, r = N: a single tile per column -> whole-column kernel
     (8192, 1200, 1024, 17, COL),    # N = 2^13, many columns: whole-column kernel
+    (1 << 20, 2, 14000, 20, V3),    # v3 with rpt/8 = 8 shared-gather slots (56 load slots: odd chunk count)
+    ((1 << 18) + 12344, 3, 12000, 21, V3),  # the same slot count with a ragged tail tile (ld % 4 == 0)
 ])
 def test_dense_random_parity(lib, n, c, r, seed, kern):
     from oracle import srht as osr

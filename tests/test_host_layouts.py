@@ -24,7 +24,8 @@ def v3_mid(x):
 
 @pytest.mark.parametrize("N,r,seed,want_pairs", [(1 << 26, 16384, 0, 16), (1 << 20, 8192, 0, 4),
                                                  (1 << 20, 16384, 5, 16), (1 << 18, 4096, 1, 0),
-                                                 (1 << 16, 1024, 2, 0), (1 << 20, 5000, 3, 0)])
+                                                 (1 << 16, 1024, 2, 0), (1 << 20, 5000, 3, 0),
+                                                 (1 << 20, 14000, 3, 8)])
 def test_v3_shared_gather_dealing(lib, N, r, seed, want_pairs):
     K = osr.plan_samples(seed, 0, N, r).astype(np.int32)
     rpt = 8 if r <= 2048 else 16 if r <= 4096 else 32 if r <= 8192 else 64
