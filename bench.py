@@ -674,11 +674,36 @@ def plan_has_reduce(plan):
     return plan.workspace_bytes(1) > 0
 
 
+def bind_near_gpu(device):
+    """Restrict this process to the CPUs NVML reports as local to `device` (so the pinned host
+    buffers are first-touched, and DMA'd, on the GPU's NUMA node).  Returns (previous affinity, note)."""
+    prev = os.sched_getaffinity(0)
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            bus = torch.cuda.get_device_properties(device).pci_bus_id  # torch >= 2.x
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus if isinstance(bus, bytes) else bus.encode())
+        except Exception:
+            h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        words = (os.cpu_count() + 63) // 64
+        mask = pynvml.nvmlDeviceGetCpuAffinity(h, words)
+        cpus = {64 * w + b for w, m in enumerate(mask) for b in range(64) if (m >> b) & 1} & prev
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return prev, "%d host cpus local to the GPU (NVML affinity)" % len(cpus)
+    except Exception as e:  # no NVML affinity: keep the current binding
+        return prev, "unbound (%s)" % type(e).__name__
+    return prev, "unbound"
+
+
 def measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device, peers=None):
     """Host-buffer end-to-end: pinned host [A|b] shard -> device -> sketch -> host, every step."""
     import psutil
     import torch
     import torch.distributed as dist
+    prev_aff, binding = bind_near_gpu(device)
     need = 4 * n * cl
     avail = psutil.virtual_memory().available
     cols = cl
@@ -730,7 +755,9 @@ def measure_e2e(args, plan, Ml, n, r, c, cl, world, rank, device, peers=None):
            "d2h_bytes_per_step": d2h, "seconds_per_step": sec, "api": api}
     if cols < cl:
         e2e["sample"] = "%d of %d columns per rank (host RAM %.0f GB available)" % (cols, cl, avail / 1e9)
+    e2e["host_binding"] = binding
     del host
+    os.sched_setaffinity(0, prev_aff)
     return e2e
 
 
