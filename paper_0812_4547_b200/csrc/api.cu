@@ -159,44 +159,160 @@ int choose_pairs3(const std::vector<int32_t>& K, int rpt) {
   return 0;
 }
 
+// Gather-bank dealing.  A warp-wide gather (load slot l of warp w, 32 lanes) costs one shared-memory
+// wavefront per distinct z word in its most used bank; lanes that read the same word are served by
+// one broadcast.  So the samples of one z word that a row takes form a unit (one word, k lanes), and a
+// row costs one wavefront when its units come from distinct banks.  (1) Pair selection: 256 P3 pairs
+// (two samples of one k_lo per load) are taken one at a time from the bank whose single units most
+// exceed its share of the single rows relative to its pair units' share of the pair rows, preferring
+// words with exactly two samples left (the pair removes a single unit).  (2) Rows are filled one at a
+// time with at most one unit per bank, banks with the most units left first (the largest unit that
+// fits; a unit larger than the room left is split), then any room left from the bank with the most
+// lanes left.  Config 5's plan: 384 wavefronts per tile, the one-per-instruction floor (round-robin
+// dealing by bank: 511); config 4: 233 (floor 224; was 346).  Empty lanes read their row's first word.
+namespace {
+struct GUnit {
+  int lo, lanes;
+};
+// rows x 32 lanes -> k_lo of the lane's word (-1: empty)
+void deal_rows_by_bank(std::vector<std::vector<GUnit>>& units, int nrows, std::vector<int>& lane_lo) {
+  lane_lo.assign((size_t)nrows * 32, -1);
+  auto by_lanes = [](const GUnit& a, const GUnit& b) { return a.lanes > b.lanes; };
+  for (auto& u : units) std::stable_sort(u.begin(), u.end(), by_lanes);
+  int order[32];
+  int64_t rem = 0;
+  for (const auto& u : units)
+    for (const GUnit& g : u) rem += g.lanes;
+  for (int row = 0; row < nrows; ++row) {
+    // lanes for this row: an even share of what is left (32 when every slot is used)
+    const int64_t share = (rem + (nrows - row) - 1) / (nrows - row);
+    int cap = share < 32 ? (int)share : 32, fill = 0;
+    rem -= cap;
+    auto put = [&](int lo, int k) {
+      for (int i = 0; i < k; ++i) lane_lo[(size_t)row * 32 + fill++] = lo;
+      cap -= k;
+    };
+    for (int b = 0; b < 32; ++b) order[b] = b;
+    std::stable_sort(order, order + 32, [&](int a, int b) { return units[a].size() > units[b].size(); });
+    for (int oi = 0; oi < 32 && cap > 0; ++oi) {
+      std::vector<GUnit>& u = units[order[oi]];
+      if (u.empty()) continue;
+      size_t i = 0;
+      while (i < u.size() && u[i].lanes > cap) ++i;
+      if (i == u.size()) {  // split the largest unit
+        GUnit g = u[0];
+        g.lanes -= cap;
+        put(g.lo, cap);
+        u.erase(u.begin());
+        u.insert(std::upper_bound(u.begin(), u.end(), g, by_lanes), g);
+      } else {
+        put(u[i].lo, u[i].lanes);
+        u.erase(u.begin() + (std::ptrdiff_t)i);
+      }
+    }
+    while (cap > 0) {  // room left: the bank with the most lanes left (a second word of that bank)
+      int best = -1, bl = 0;
+      for (int b = 0; b < 32; ++b) {
+        int l = 0;
+        for (const GUnit& g : units[b]) l += g.lanes;
+        if (l > bl) {
+          bl = l;
+          best = b;
+        }
+      }
+      if (best < 0) {
+        rem += cap;
+        break;
+      }
+      GUnit& g = units[best][0];
+      const int k = g.lanes < cap ? g.lanes : cap;
+      put(g.lo, k);
+      g.lanes -= k;
+      if (g.lanes == 0) units[best].erase(units[best].begin());
+    }
+  }
+}
+}  // namespace
+
 void deal_v3_pairs(const std::vector<int32_t>& K, int rpt, int P3, std::vector<int32_t>& acc_t,
                    std::vector<uint32_t>& meta_off) {
+  constexpr int LO = 1 << 14;
   const int L = rpt - P3;
+  const int prows = P3 * 8, srows = (L - P3) * 8;
   acc_t.assign((size_t)rpt * 256, -1);
   meta_off.assign((size_t)256 * L, 0u);
-  std::vector<std::vector<int32_t>> by_lo(1 << 14);
-  for (size_t t = 0; t < K.size(); ++t) by_lo[K[t] & ((1 << 14) - 1)].push_back((int32_t)t);
-  // pairs (by bank of the shared address), then singles (by bank)
-  std::vector<std::vector<std::pair<int32_t, int32_t>>> pb(32);
-  std::vector<std::vector<int32_t>> sb(32);
-  int64_t need = (int64_t)256 * P3;
-  for (int lo = 0; lo < (1 << 14); ++lo) {
-    const std::vector<int32_t>& g = by_lo[lo];
-    const int bank = srht::v3_mid(lo) & 31;
-    size_t i = 0;
-    for (; i + 1 < g.size() && need > 0; i += 2, --need) pb[bank].push_back({g[i], g[i + 1]});
-    for (; i < g.size(); ++i) sb[bank].push_back(g[i]);
+  std::vector<std::vector<int32_t>> by_lo(LO);
+  for (size_t t = 0; t < K.size(); ++t) by_lo[K[t] & (LO - 1)].push_back((int32_t)t);
+  auto bank = [](int lo) { return srht::v3_mid(lo) & 31; };
+  // (1) pair selection
+  std::vector<int> left(LO), npair(LO, 0);
+  std::vector<std::vector<int>> cand(32);  // words with >= 2 samples
+  double su[32] = {}, pu[32] = {};
+  for (int lo = 0; lo < LO; ++lo) {
+    left[lo] = (int)by_lo[lo].size();
+    if (left[lo] > 0) su[bank(lo)] += 1.0;
+    if (left[lo] >= 2) cand[bank(lo)].push_back(lo);
   }
-  // pair rows (l < P3, warp w): row = l * 8 + w; single rows (l >= P3): row = (l - P3) * 8 + w
-  const int prow = P3 * 8, srow = (L - P3) * 8;
-  std::vector<int> pfill(prow > 0 ? prow : 1, 0), sfill(srow > 0 ? srow : 1, 0);
-  int64_t i = 0;
-  for (int b = 0; b < 32; ++b)
-    for (const auto& pr : pb[b]) {
-      const int row = (int)(i++ % prow), lane = pfill[row]++;
-      const int l = row / 8, c = (row % 8) * 32 + lane;
-      acc_t[(size_t)(2 * l) * 256 + c] = pr.first;
-      acc_t[(size_t)(2 * l + 1) * 256 + c] = pr.second;
-      meta_off[(size_t)c * L + l] = (uint32_t)srht::v3_mid(K[pr.first] & ((1 << 14) - 1)) * 4u;
+  for (int64_t k = 0; k < (int64_t)256 * P3; ++k) {
+    int bb = -1, blo = -1;
+    double bs = 0.0;
+    for (int b = 0; b < 32; ++b) {
+      int w = -1;
+      for (int lo : cand[b])  // a word with exactly two left, else the one with the most left
+        if (left[lo] >= 2 && (w < 0 || (left[lo] == 2) > (left[w] == 2) ||
+                              ((left[lo] == 2) == (left[w] == 2) && left[lo] > left[w])))
+          w = lo;
+      if (w < 0) continue;
+      const double sc = su[b] / (srows > 0 ? srows : 1) - pu[b] / prows + (left[w] == 2 ? 1e-3 : 0.0);
+      if (bb < 0 || sc > bs) {
+        bb = b;
+        blo = w;
+        bs = sc;
+      }
     }
-  i = 0;
-  for (int b = 0; b < 32; ++b)
-    for (int32_t t : sb[b]) {
-      const int row = (int)(i++ % srow), lane = sfill[row]++;
-      const int l = P3 + row / 8, c = (row % 8) * 32 + lane;
-      acc_t[(size_t)(P3 + l) * 256 + c] = t;  // accumulator 2 P3 + (l - P3)
-      meta_off[(size_t)c * L + l] = (uint32_t)srht::v3_mid(K[t] & ((1 << 14) - 1)) * 4u;
+    if (bb < 0) break;  // (choose_pairs3 guarantees enough pairs)
+    if (left[blo] == 2) su[bb] -= 1.0;
+    if (npair[blo] == 0) pu[bb] += 1.0;
+    ++npair[blo];
+    left[blo] -= 2;
+  }
+  // (2) rows
+  std::vector<std::vector<GUnit>> pun(32), sun(32);
+  for (int lo = 0; lo < LO; ++lo) {
+    if (npair[lo] > 0) pun[bank(lo)].push_back({lo, npair[lo]});
+    if (left[lo] > 0) sun[bank(lo)].push_back({lo, left[lo]});
+  }
+  std::vector<int> cursor(LO, 0);
+  std::vector<int> lane_lo;
+  if (prows > 0) {
+    deal_rows_by_bank(pun, prows, lane_lo);
+    for (int row = 0; row < prows; ++row) {
+      const int l = row / 8, w = row % 8;
+      for (int lane = 0; lane < 32; ++lane) {
+        const int c = w * 32 + lane;
+        const int lo = lane_lo[(size_t)row * 32 + lane];
+        const int rl = lo >= 0 ? lo : lane_lo[(size_t)row * 32];
+        if (rl >= 0) meta_off[(size_t)c * L + l] = (uint32_t)srht::v3_mid(rl) * 4u;
+        if (lo < 0) continue;
+        acc_t[(size_t)(2 * l) * 256 + c] = by_lo[lo][cursor[lo]++];
+        acc_t[(size_t)(2 * l + 1) * 256 + c] = by_lo[lo][cursor[lo]++];
+      }
     }
+  }
+  if (srows > 0) {
+    deal_rows_by_bank(sun, srows, lane_lo);
+    for (int row = 0; row < srows; ++row) {
+      const int l = P3 + row / 8, w = row % 8;
+      for (int lane = 0; lane < 32; ++lane) {
+        const int c = w * 32 + lane;
+        const int lo = lane_lo[(size_t)row * 32 + lane];
+        const int rl = lo >= 0 ? lo : lane_lo[(size_t)row * 32];
+        if (rl >= 0) meta_off[(size_t)c * L + l] = (uint32_t)srht::v3_mid(rl) * 4u;
+        if (lo < 0) continue;
+        acc_t[(size_t)(P3 + l) * 256 + c] = by_lo[lo][cursor[lo]++];  // accumulator 2 P3 + (l - P3)
+      }
+    }
+  }
 }
 
 // Whole-column kernel gather order for one problem (r <= 1024 kept rows K, N = 2^13): out[COL_SLOTS]
@@ -585,6 +701,9 @@ srht_status srht_plan_create_ex(int64_t n, int64_t d, int64_t r, uint64_t seed, 
   P->threads = (int)(P->B / 32);
   const int64_t per = (r + P->threads - 1) / P->threads;
   P->rpt = per <= 4 ? 4 : per <= 8 ? 8 : per <= 16 ? 16 : 32;
+#ifdef SRHT_V1_MAX_RPT  // experiment: fewer accumulators per thread, more sample groups (CTAs) per tile
+  if (P->rpt > SRHT_V1_MAX_RPT && P->B >= (int64_t(1) << 13)) P->rpt = SRHT_V1_MAX_RPT;
+#endif
   P->groups = (r + (int64_t)P->rpt * P->threads - 1) / ((int64_t)P->rpt * P->threads);
   P->words64 = P->N_eff / 64;
   P->scale = (float)(1.0 / std::sqrt((double)P->r_target));

@@ -483,9 +483,11 @@ def test_v3_shared_gather_layout(lib, n, r, want_pairs):
     for l in range(nl):
         qs = (2 * l, 2 * l + 1) if l < P else (P + l,)
         used[:, l] = np.any(valid[:, list(qs)], axis=1)
-    banks = np.where(used, (meta // 4 % 32).astype(np.int64), -1).T.reshape(nl, 8, 32).reshape(-1, 32)
-    worst = max(np.bincount(row[row >= 0], minlength=32).max() if (row >= 0).any() else 0 for row in banks)
-    assert worst <= 2, worst
+    words = np.where(used, (meta // 4).astype(np.int64), -1).T.reshape(nl, 8, 32).reshape(-1, 32)
+    # a warp-wide gather costs one wavefront per distinct word in its most used bank (same-word lanes
+    # are one broadcast); the plan's bank dealing stays within 2% + 4 of one per instruction
+    cost = [np.bincount(np.unique(row[row >= 0]) % 32, minlength=32).max() for row in words if (row >= 0).any()]
+    assert sum(cost) <= 1.02 * len(words) + 4, (sum(cost), len(words))
 
 
 # ---- row shards: unscaled FP64 partials per shard, summed by the caller ----

@@ -52,10 +52,23 @@ def test_v3_shared_gather_dealing(lib, N, r, seed, want_pairs):
             assert np.array_equal(lo[ts[0, both]], lo[ts[1, both]])
         t0 = np.where(ts[0] >= 0, ts[0], ts[-1])
         assert np.array_equal(meta[used, l], 4 * v3_mid(lo[t0[used]]))  # byte offset of z[k_lo]
-        banks[l, used] = v3_mid(lo[t0[used]]) % 32
+        banks[l, used] = v3_mid(lo[t0[used]])
     rows = banks.reshape(nl, 8, 32).reshape(-1, 32)  # warp-wide loads: (slot, warp) x 32 lanes
-    worst = max(np.bincount(row[row >= 0], minlength=32).max() for row in rows if (row >= 0).any())
-    assert worst <= 2, worst
+    # a warp-wide LDS costs one wavefront per distinct word in its most used bank (lanes reading the
+    # same word are served by one broadcast)
+    cost = [np.bincount(np.unique(row[row >= 0]) % 32, minlength=32).max() for row in rows if (row >= 0).any()]
+    assert max(cost) <= 8, max(cost)  # the excess of an overfull bank may meet in one row
+    # bank dealing: within 2% + 4 of the one-wavefront-per-instruction floor (round-robin dealing by
+    # bank gave 511 for config 5's plan and 346 for config 4's)
+    assert sum(cost) <= 1.02 * len(rows) + 4, (sum(cost), len(rows))
+    # empty lanes read a word their row already reads (no extra wavefront)
+    for l in range(nl):
+        for w in range(8):
+            lanes = slice(32 * w, 32 * w + 32)
+            qs = (2 * l, 2 * l + 1) if l < P else (P + l,)
+            empty = (acc[list(qs)][:, lanes] < 0).all(axis=0)
+            if empty.any() and (~empty).any():
+                assert set(meta[lanes, l][empty]) <= set(meta[lanes, l][~empty])
     # shared gathers cut the loads per thread to rpt - P
     assert nl * 256 >= r - 256 * P
 
