@@ -79,10 +79,15 @@ constexpr int NQ = V3_QSPLIT ? 4 : 1;
 #define V3_SPLIT_ISSUE 1
 #endif
 constexpr bool SPLIT = V3_SPLIT_ISSUE && NQ == 4;
+// Quarters copied by the refill (the producer copies the rest): one for r = 16384 (RPT 64: config 5,
+// 7.08 vs 7.33 ms with two), two for smaller r (RPT <= 32: config 4, 0.434 vs 0.447 ms back to back;
+// profiles/r02c_ab_params.jsonl).
 #ifndef V3_REFILL_Q
-#define V3_REFILL_Q 1  // quarters copied by the refill (the producer copies the rest)
+#define V3_REFILL_Q 0  // 0: by RPT as above
 #endif
-constexpr int NREF = SPLIT ? V3_REFILL_Q : NQ;
+__host__ __device__ constexpr int nref_for(int rpt) {
+  return !SPLIT ? NQ : V3_REFILL_Q > 0 ? V3_REFILL_Q : (rpt >= 64 ? 1 : 2);
+}
 // control block: FULL mbarriers [0, 8 NQ NBUF), TMEM address [96,100), EMPTY mbarriers
 // [104,128), slot states [128,..)
 constexpr int CTRL_TMEM = 96, CTRL_EMPTY = 104, CTRL_SLOTS = 128, CTRL_TFULL = 384, CTRL_BYTES = 512;
@@ -275,7 +280,7 @@ __device__ __forceinline__ bool flat_tile(const V3Params& P, int f, int& tile, c
   return true;
 }
 
-template <int DBG>
+template <int DBG, int NREF>
 __device__ __forceinline__ void tma_issue(const V3Params& P, SlotState& st, int b, unsigned char* smem) {
   Cursor c = st.cur;
   int tile;
@@ -379,6 +384,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
   SlotState* slots = reinterpret_cast<SlotState*>(smem + CTRL_OFF + CTRL_SLOTS);
   static_assert(PAIRS % 2 == 0 && 2 * PAIRS <= RPT && (RPT - PAIRS) % 4 == 0, "pair slots");
   constexpr int MW = RPT - PAIRS;                    // gather byte offsets (TMEM columns) per consumer thread
+  constexpr int NREF = nref_for(RPT);
   // TMEM columns allocated: raw tiles (TMEM_RAW) + gather offsets (two consumer warps per lane quarter)
   constexpr int TCOLS = V3_TMEM_RAW ? 512 : META_PER_BUF ? pow2_at_least(2 * NBUF * MW) : ((2 * MW) < 32 ? 32 : 2 * MW);
   const int tid = threadIdx.x;
@@ -636,7 +642,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
         slots[b].f = b;
         cursor_next_active(P, c0);
       }
-      for (int b = 0; b < NBUF; ++b) tma_issue<DBG>(P, slots[b], b, smem);
+      for (int b = 0; b < NBUF; ++b) tma_issue<DBG, NREF>(P, slots[b], b, smem);
     }
     float acc[RPT];
 #pragma unroll
@@ -724,13 +730,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
               // acquire the other warps' arrivals (their reads of buffer b) before the
               // refill overwrites it: the phase is complete, so this wait returns at once
               mbar_wait(smem_u32(smem + CTRL_OFF + CTRL_EMPTY + 8 * b), (uint32_t)((f / NBUF) & 1));
-              tma_issue<DBG>(P, slots[b], b, smem);
+              tma_issue<DBG, NREF>(P, slots[b], b, smem);
             }
 #else
             const int done = atomicAdd(&slots[b].count, 1);
             if (done == NCONS / 32 - 1) {
               slots[b].count = 0;
-              tma_issue<DBG>(P, slots[b], b, smem);
+              tma_issue<DBG, NREF>(P, slots[b], b, smem);
             }
 #endif
           }
