@@ -47,7 +47,7 @@ def parse():
                     help="fp32: the throughput path; fp64: the FP64-accumulation parity mode "
                          "(DESIGN.md reading R14), which meets the 1e-6 end-to-end gate on configs 4/5")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--sustain-seconds", type=float, default=1.0,
                     help="after the timed steps, run back to back for about this long and report the "
                          "steady-state step (the 1000 W board cap engages after ~50 ms); 0 = skip")
