@@ -3,6 +3,7 @@
 
 #include <cmath>
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -563,6 +564,12 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
       vp.debug = srht::g_debug_mode;
       e = srht::launch_sketch_tma(P, vp, st);
       srht::g_last_kernel = 3;
+#ifdef V3_SYNC_CHECK  // experiment build: name the kernel an asynchronous fault comes from
+      if (e == cudaSuccess) {
+        const cudaError_t se = cudaStreamSynchronize(st);
+        if (se != cudaSuccess) fprintf(stderr, "V3_SYNC_CHECK k_sketch_tma rpt %d: %s\n", P->rpt2, cudaGetErrorString(se));
+      }
+#endif
     } else {
       srht::WsParams wp;
       std::memset(&wp, 0, sizeof(wp));
@@ -592,6 +599,12 @@ srht_status run(const srht_plan* P, srht::SketchParams& sp, void* ws, size_t ws_
     if (e != cudaSuccess) return SRHT_ECUDA;
     if (v3) {  // slot-order partials, always reduced (also for a single slab)
       if (srht::launch_reduce_v3(rp, P->d_ttab3, P->rpt2, 14 + P->log_j2, st) != cudaSuccess) return SRHT_ECUDA;
+#ifdef V3_SYNC_CHECK
+      {
+        const cudaError_t se = cudaStreamSynchronize(st);
+        if (se != cudaSuccess) fprintf(stderr, "V3_SYNC_CHECK k_reduce_v3 rpt %d: %s\n", P->rpt2, cudaGetErrorString(se));
+      }
+#endif
     } else if (!direct && srht::launch_reduce(rp, 14 + P->log_j2, st) != cudaSuccess) {
       return SRHT_ECUDA;
     }

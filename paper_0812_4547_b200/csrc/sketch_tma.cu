@@ -386,7 +386,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sketch_tma(const __grid_constan
   constexpr int MW = RPT - PAIRS;                    // gather byte offsets (TMEM columns) per consumer thread
   constexpr int NREF = nref_for(RPT);
   // TMEM columns allocated: raw tiles (TMEM_RAW) + gather offsets (two consumer warps per lane quarter)
-  constexpr int TCOLS = V3_TMEM_RAW ? 512 : META_PER_BUF ? pow2_at_least(2 * NBUF * MW) : ((2 * MW) < 32 ? 32 : 2 * MW);
+#ifndef V3_TCOLS_ALL
+#define V3_TCOLS_ALL 0  // experiment: allocate all 512 TMEM columns for every RPT
+#endif
+  constexpr int TCOLS = (V3_TMEM_RAW || V3_TCOLS_ALL) ? 512 : META_PER_BUF ? pow2_at_least(2 * NBUF * MW) : ((2 * MW) < 32 ? 32 : 2 * MW);
   const int tid = threadIdx.x;
 
   // ---------------- setup (all threads) ----------------

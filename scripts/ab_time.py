@@ -24,7 +24,13 @@ for cfg in cfgs:
     c = d + 1
     M = torch.empty((c, n), dtype=torch.float32, device="cuda").t()
     srht.gen_uniform(0, 0, M)
+    if os.environ.get("AB_SYNC"):  # stress runs: name the stage an asynchronous fault surfaces in
+        torch.cuda.synchronize()
+        print("progress: config %d inputs generated" % cfg, file=sys.stderr, flush=True)
     plan = srht.Plan(n, d, r, 0)
+    if os.environ.get("AB_SYNC"):
+        torch.cuda.synchronize()
+        print("progress: config %d plan built" % cfg, file=sys.stderr, flush=True)
     ws = plan.workspace(c)
     out = torch.empty((c, r), device="cuda").t()
 
@@ -41,10 +47,14 @@ for cfg in cfgs:
         lib.srht_profile_stop(arr, k, ctypes.byref(cnt))
         return [arr[i] for i in range(cnt.value)]
 
+    print("progress: config %d first sketches" % cfg, file=sys.stderr, flush=True)
     run(3, 0)
+    print("progress: config %d first sketches done" % cfg, file=sys.stderr, flush=True)
     ref_out = out.clone()
     alone = run(6, 0.3)
+    print("progress: config %d alone runs done" % cfg, file=sys.stderr, flush=True)
     b2b = run(20 if cfg == 5 else 200, 0)
+    print("progress: config %d back-to-back runs done" % cfg, file=sys.stderr, flush=True)
     res["c%d" % cfg] = {"alone_med": statistics.median(alone), "b2b_first10": statistics.mean(b2b[:10]),
                         "b2b_last10": statistics.mean(b2b[-10:]), "kernel": lib.srht_debug_last_kernel(),
                         "deterministic": bool(torch.equal(out, ref_out))}
@@ -58,4 +68,7 @@ for cfg in cfgs:
             res["c4_err_over_bound_col%d" % j] = float(np.abs(got - ref).max() / bound)
     del M, out, ws, plan
     torch.cuda.empty_cache()
+    if os.environ.get("AB_SLEEP"):  # stress runs: let the clocks recover between configurations
+        torch.cuda.synchronize()
+        time.sleep(float(os.environ["AB_SLEEP"]))
 print(json.dumps(res), flush=True)
