@@ -233,8 +233,11 @@ __global__ void __launch_bounds__(416) k_gram_tri(int64_t r, int64_t c, int64_t 
 // Each element is computed once in the upper triangle and mirrored (exactly symmetric).
 constexpr int MB = 64, MKT = 32, MPK = MKT + 4;
 
+#ifndef GRAM_MMA_MINB
+#define GRAM_MMA_MINB 4
+#endif
 template <bool VEC>
-__global__ void __launch_bounds__(128, 4) k_gram_mma(int64_t r, int64_t c, int64_t batch, const float* __restrict__ SM,
+__global__ void __launch_bounds__(128, GRAM_MMA_MINB) k_gram_mma(int64_t r, int64_t c, int64_t batch, const float* __restrict__ SM,
                                                   int64_t ldsm, int64_t stride_sm, double* __restrict__ G, int64_t ldg,
                                                   int64_t stride_g, int nb, int splits, int64_t kchunk,
                                                   double* __restrict__ part) {
@@ -409,7 +412,7 @@ constexpr int SMC = 128, SNT = SMC / 8;  // max columns, max tile rows
 #define GRAM_DB 1
 #endif
 #ifndef GRAM_SMALL_MINB
-#define GRAM_SMALL_MINB 1
+#define GRAM_SMALL_MINB 2  // 2 CTAs per SM at 128 registers, no spills (config 2: 2.16 -> 1.83 ms, bit-identical)
 #endif
 template <bool VEC>
 __global__ void __launch_bounds__(256, GRAM_SMALL_MINB) k_gram_mma_small(int64_t r, int64_t c, int64_t batch,
